@@ -1,0 +1,170 @@
+/*
+ * tsb200.h -- C-ABI of the B200-native MOSS per-step vehicle loop.
+ *
+ * The reference (trafficsim, pure Python) has no FFI: the hot path sits behind
+ * the Python class trafficsim.engine.world.World (engine/world.py:111-834,
+ * re-exported at engine/__init__.py:18-27).  This header is the boundary that
+ * replaces it: paper_2405_12520_b200.world.World (the drop-in Python class)
+ * binds these symbols with ctypes.  Each entry point names the reference
+ * interface it replaces.  All calls are synchronous with respect to the
+ * engine's CUDA stream unless stated; an engine is single-threaded (one
+ * caller, control calls only between steps).
+ *
+ * Inputs are plain host pointers and sizes; they are copied on create.
+ * Outputs go to caller-allocated buffers.  No torch types cross this line.
+ *
+ * Return codes: TSB_OK (0) or a negative code; tsb_last_error() gives the
+ * thread-local message.  TSB_EINVAL / TSB_ERANGE map to InputError,
+ * everything else to EngineError (a TrafficSimError).
+ */
+#ifndef TSB200_H
+#define TSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSB_OK 0
+#define TSB_EINVAL (-1) /* bad argument            -> InputError  */
+#define TSB_ERANGE (-2) /* index out of range      -> InputError  */
+#define TSB_ECUDA (-3)  /* CUDA runtime failure    -> EngineError */
+#define TSB_ECAP (-4)   /* device capacity exceeded -> EngineError */
+#define TSB_EHOST (-5)  /* host-side failure (alloc, internal) */
+
+#define TSB_KIND_ROAD 0
+#define TSB_KIND_CONNECTOR 1
+#define TSB_KIND_NONE (-1)
+
+#define TSB_STATUS_WAITING 0
+#define TSB_STATUS_DRIVING 1
+#define TSB_STATUS_FINISHED 2
+#define TSB_STATUS_DROPPED 3
+
+/* Lane-level network, SoA; lane index == reference lane id.
+ * Replaces the per-lane tables of World.__init__ (world.py:127-179). */
+typedef struct tsb_network {
+  int32_t n_lanes;
+  const double* lane_len;
+  const double* lane_cap;        /* max_speed */
+  const int8_t* lane_kind;       /* TSB_KIND_* */
+  const uint8_t* lane_open;      /* restriction == "open" */
+  const int32_t* lane_left;      /* -1 = none */
+  const int32_t* lane_right;
+  const int32_t* lane_road;      /* road index of a road lane, -1 for connectors */
+  const int32_t* lane_junction;  /* junction index of a connector, -1 for road lanes */
+  const int32_t* lane_pred1;     /* connector: its single predecessor road lane */
+  const int32_t* lane_succ1;     /* connector: its single successor road lane */
+  const int32_t* succ_off;       /* [n_lanes+1] CSR of lane.successors (sorted) */
+  const int32_t* succ;
+  const int32_t* pred_off;       /* [n_lanes+1] CSR of lane.predecessors (sorted) */
+  const int32_t* pred;
+  int32_t n_roads;
+  const int32_t* road_lane_off;  /* [n_roads+1] CSR of net.roads[rid] (leftmost first) */
+  const int32_t* road_lanes;
+  int32_t n_junctions;
+  const uint8_t* junc_signal;    /* 1 = has a signal program */
+  const int32_t* junc_phase_off; /* [n_junctions+1] CSR into phase_dur */
+  const double* phase_dur;
+  const uint64_t* lane_green_mask; /* connector: bit p set iff green in phase p */
+  const int32_t* junc_phase0;      /* initial state (signals.initial_state) */
+  const double* junc_elapsed0;
+} tsb_network;
+
+/* Trips in ascending-id order: index == vix (dense vehicle index).
+ * Replaces list[Trip] (demand.py:47-53) as consumed by World (world.py:181-198). */
+typedef struct tsb_trips {
+  int32_t n;
+  const uint64_t* key;  /* id & (2^64-1): the keyed-RNG vehicle key (rng.py:35) */
+  const int32_t* origin_lane;
+  const double* origin_s;
+  const int32_t* dest_lane;
+  const double* departure;
+} tsb_trips;
+
+/* EngineConfig (params.py:48-83) flattened; seed = World seed & (2^64-1). */
+typedef struct tsb_params {
+  double dt, lookahead;
+  double idm_v0, idm_T, idm_a_max, idm_b, idm_delta, idm_s0;
+  double mobil_politeness, mobil_threshold, mobil_b_safe, mobil_eval_prob;
+  double vehicle_length, speed_window, amber, s0_floor, mp_interval, mp_min_green;
+  int32_t controller; /* 0 = fixed, 1 = max_pressure */
+  int32_t pow_mode;   /* 0 = correctly-rounded powers (device) */
+  uint64_t seed;
+} tsb_params;
+
+/* StepReport (world.py:72-80) plus engine counters. */
+typedef struct tsb_report {
+  double time;
+  int64_t step_no;
+  int64_t driving, waiting, finished, dropped, injected_now, finished_now;
+  int64_t vehicle_updates; /* cumulative, world.py:663 */
+  int64_t reverts_last;    /* collision-sweep reverts in the last step */
+} tsb_report;
+
+typedef struct tsb_engine tsb_engine;
+
+/* World.__init__ (world.py:112-206): upload network/trips, compute routes on
+ * the host router (routing.py:19-107), build the step graph. */
+int tsb_create(const tsb_network* net, const tsb_trips* trips, const tsb_params* p,
+               int32_t device, tsb_engine** out);
+void tsb_destroy(tsb_engine* e); /* World.close (world.py:827-830) */
+const char* tsb_last_error(void);
+
+/* World.step() x n (world.py:659-689); report of the last step (may be NULL). */
+int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last);
+/* Current counters without stepping. */
+int tsb_report_get(tsb_engine* e, tsb_report* out);
+
+/* World.prepare() (world.py:211-242): the per-lane index.  Fills the
+ * lane-sorted snapshot (lane asc, s desc, id asc): lane_start[n_lanes+1] and
+ * per-vehicle vix/lane/road_pos/s/v arrays of capacity >= n_driving. */
+int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* vix,
+              int32_t* lane, int32_t* road_pos, double* s, double* v);
+/* Per-vix status (TSB_STATUS_*) and finish time; World.get_vehicle (world.py:706-714). */
+int tsb_status(tsb_engine* e, uint8_t* status, double* finish_time);
+/* World.finished (world.py:199, 491): arrivals appended since index `since`
+ * in reference order (step, then id).  *n_out = number written. */
+int tsb_finished(tsb_engine* e, int64_t since, int64_t cap, int32_t* vix, double* finish_time,
+                 int64_t* n_out);
+/* Road aggregate (world.py:649-657): per (road, window) speed sum and count,
+ * row-major [n_roads][n_windows]; windows beyond the engine's range are 0. */
+int tsb_road_acc(tsb_engine* e, int32_t n_windows, double* sum, int64_t* count);
+/* World.min_front_gap (world.py:694-704), computed on device. */
+int tsb_min_front_gap(tsb_engine* e, double* out);
+
+/* Control surface, between steps only (world.py:716-740). */
+int tsb_set_lane(tsb_engine* e, int32_t lane, double max_speed, int32_t open);
+int tsb_set_signal_phase(tsb_engine* e, int32_t junction, int32_t phase);
+/* Signal state per junction: phase, elapsed (signals.py:22-26). */
+int tsb_signal_state(tsb_engine* e, int32_t* phase, double* elapsed);
+
+/* Host router (routing.py:70-107): lane path origin -> dest on the engine's
+ * current lane state.  Returns TSB_OK and *n = 0 when unroutable. */
+int tsb_route(tsb_engine* e, int32_t origin, int32_t dest, int32_t cap, int32_t* lanes,
+              int32_t* n, double* cost);
+
+/* Standalone router (no device): used by demand generators and tests. */
+typedef struct tsb_router tsb_router;
+int tsb_router_create(const tsb_network* net, tsb_router** out);
+void tsb_router_destroy(tsb_router* r);
+int tsb_router_route(tsb_router* r, int32_t origin, int32_t dest, int32_t cap, int32_t* lanes,
+                     int32_t* n, double* cost);
+/* reach[k*n_lanes + l] = 1 iff lane l reaches dests[k] (dist_to keys). */
+int tsb_router_reach(tsb_router* r, int32_t n_dests, const int32_t* dests, uint8_t* reach);
+
+/* Measurement hooks for bench.py: run n steps launching each kernel with
+ * CUDA events on the engine stream; kernel_ms[k] = mean per-step duration of
+ * kernel class k, names via tsb_kernel_name(k). Returns number of classes. */
+int tsb_profile_steps(tsb_engine* e, int32_t n_steps, int32_t cap, double* kernel_ms);
+const char* tsb_kernel_name(int32_t k);
+/* Device time (ms) of n graph-replayed steps bracketed by CUDA events. */
+int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms);
+/* Kernel launches issued per step (for the bench's gpu_launches claim). */
+int tsb_launches_per_step(tsb_engine* e, int32_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
