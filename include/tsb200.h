@@ -122,8 +122,12 @@ int tsb_report_get(tsb_engine* e, tsb_report* out);
  * per-vehicle vix/lane/road_pos/s/v arrays of capacity >= n_driving. */
 int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* vix,
               int32_t* lane, int32_t* road_pos, double* s, double* v);
-/* Per-vix status (TSB_STATUS_*) and finish time; World.get_vehicle (world.py:706-714). */
-int tsb_status(tsb_engine* e, uint8_t* status, double* finish_time);
+/* Per-vix status (TSB_STATUS_*), finish time, and for finished vehicles the
+ * last committed state (lane, s, v, road_pos) before the arrival step, which
+ * is what World.get_vehicle reports for them (world.py:488-494, 706-714).
+ * Any output pointer may be NULL. */
+int tsb_status(tsb_engine* e, uint8_t* status, double* finish_time, int32_t* last_lane, double* last_s,
+               double* last_v, int32_t* last_rp);
 /* World.finished (world.py:199, 491): arrivals appended since index `since`
  * in reference order (step, then id).  *n_out = number written. */
 int tsb_finished(tsb_engine* e, int64_t since, int64_t cap, int32_t* vix, double* finish_time,

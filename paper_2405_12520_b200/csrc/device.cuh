@@ -1,0 +1,244 @@
+// device.cuh -- device data layout and the per-vehicle model arithmetic.
+//
+// Every floating-point expression keeps CPython's evaluation order and
+// rounding (the reference is trafficsim/engine/*.py); the library is built
+// with --fmad=false so nvcc never contracts a*b+c into an FMA.  The only FMA
+// calls below are explicit, inside the double-double power, where they are
+// exact error-free transforms.
+#pragma once
+#include <cstdint>
+
+#include "../../include/tsb200.h"
+
+namespace tsb {
+
+// ---------------------------------------------------------------- layout
+
+// One driving vehicle in a lane-sorted layout (32 B, two 16 B vectors).
+// `lane` is explicit (the CSR position implies it, but the update kernel
+// needs it without a search); `src` is the index of the vehicle in the
+// step's snapshot layout A, which carries the snapshot lane/s/rp needed by
+// the collision sweep and by reverts (world.py:501-507).
+struct __align__(16) VRec {
+  double s;
+  double v;
+  int32_t vix;
+  int32_t rp;
+  int32_t lane;
+  int32_t src;
+};
+
+// Static per-lane record (48 B) gathered by the update kernel.
+struct __align__(16) LaneRec {
+  double len;
+  double cap;
+  int32_t road;      // road index (road lane) or -1
+  int32_t junc;      // junction index (connector) or -1
+  int32_t left, right;
+  int32_t succ1;     // connector: successor road lane
+  int32_t pred1;     // connector: predecessor road lane
+  int32_t succ_off;  // CSR into succ / succ_dst_road
+  int16_t nsucc;
+  int8_t kind;
+  uint8_t open;
+};
+
+// Per-vehicle cold data, indexed by vix.
+struct __align__(16) VCold {
+  uint64_t key;       // id & (2^64-1)
+  int64_t route_off;  // into the road-index route pool
+  int32_t route_len;  // roads in roads_seq; 0 = unroutable; -1 = not computed
+  int32_t origin_lane;
+  double origin_s;
+  double depart;
+};
+
+struct JuncState {
+  int32_t phase;
+  int32_t pad;
+  double elapsed;
+  double since;
+};
+
+struct FinEntry {
+  int32_t vix;
+  int32_t pad;
+  int64_t step;
+};
+
+// Scalars that change every step (device resident so a whole step is a
+// CUDA graph with no host round trip).
+struct Dyn {
+  double time;
+  int64_t step_no;
+  int64_t vehicle_updates;
+  int64_t finished_total;
+  int64_t dropped;
+  int64_t injected_now;
+  int64_t finished_now;
+  int64_t reverts_last;
+  int32_t cur;          // which layout buffer holds the snapshot A
+  int32_t n_a;          // vehicles in A
+  int32_t n_c;          // vehicles scattered into C (post-update, excl. arrivals)
+  int32_t n_inj;        // injected this step (appended after n_c in C)
+  int32_t n_events;     // lanes whose tentative sweep hit a revert
+  int32_t n_moved;      // vehicles moved by resolve (reverted into another lane)
+  int32_t need_regroup; // membership or order changed after the sweep
+  int32_t pend_ptr;
+  int32_t n_retry;
+  int32_t n_due;
+  int32_t n_hostq;      // vehicles needing a host reroute (closures only)
+  int32_t overflow;     // sticky error flag
+  int64_t fin_log_n;
+};
+
+struct Params {
+  double dt, lookahead;
+  double v0, T, a_max, b, delta, s0;
+  double politeness, threshold, b_safe, eval_prob;
+  double L, speed_window, amber, s0_floor, mp_interval, mp_min_green;
+  double sqrt_ab2;   // 2.0 * sqrt(a_max * b), evaluated as in idm.py:29
+  int32_t controller;
+  int32_t delta_int; // delta as an integer power if integral in [1, 64], else 0
+  uint64_t seed;
+};
+
+// All device pointers of one engine (passed by value to every kernel).
+struct Ctx {
+  Params p;
+  int32_t n_lanes, n_roads, n_junc, n_trips;
+  int32_t split;  // 1 when lane closures exist: host continuation of reroutes
+  const LaneRec* lanes;
+  const int32_t* succ;
+  const int32_t* succ_dst_road;
+  const int32_t* road_lane_off;
+  const int32_t* road_lanes;
+  const int32_t* junc_phase_off;
+  const double* phase_dur;
+  const uint64_t* green;
+  const uint8_t* junc_signal;
+  const int32_t* jc_off;  // junction -> connectors CSR
+  const int32_t* jc;
+  JuncState* sig;
+  const VCold* cold;
+  const int32_t* routes;
+  uint8_t* status;
+  uint8_t* routed;
+  double* finish;
+  VRec* fin_state;  // last committed state of finished vehicles (by vix)
+  VRec* lay[2];
+  int32_t* start[2];
+  VRec* B;
+  VRec* D;
+  int32_t* cnt;
+  int32_t* cursor;
+  unsigned long long* scan_status;
+  int32_t* scan_tiles;
+  int32_t scan_tiles_cap;
+  int32_t* stage;  // scan staging (n_lanes + 1)
+  int32_t* events;
+  // resolve scratch
+  int32_t* rs_heap;
+  uint8_t* rs_inwork;
+  uint8_t* rs_touched;
+  uint8_t* rs_event;
+  uint8_t* rs_movedin;
+  int32_t* rs_moved;
+  uint8_t* rs_reverted;
+  int32_t* rs_members;
+  int32_t* rs_touched_list;
+  // injection
+  const int32_t* pend_vix;
+  const double* pend_dep;
+  int32_t* retry;
+  int32_t* retry2;
+  int32_t* due;
+  int32_t* due_grp;
+  int32_t* inj_cnt;
+  int32_t* inj_start;
+  int32_t* inj_cursor;
+  uint8_t* outcome;
+  int32_t* flag_in;
+  int32_t* flag_scan;
+  int32_t* lane_counts;  // max-pressure lane occupancy
+  // output
+  FinEntry* fin_log;
+  double* acc_sum;
+  long long* acc_cnt;
+  int32_t n_win;
+  int32_t* hostq;
+  Dyn* dyn;
+  double* scratch_d;
+};
+
+// ---------------------------------------------------------------- arithmetic
+
+__device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+
+// x**n for integer n >= 1, correctly rounded: binary powering in
+// double-double (error-free products via explicit FMA), one final rounding.
+__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double& rh, double& rl) {
+  double p = ah * bh;
+  double e = fma(ah, bh, -p);
+  e = e + (ah * bl + al * bh);
+  rh = p + e;
+  rl = e - (rh - p);
+}
+
+__device__ __forceinline__ double pow_int_cr(double x, int n) {
+  double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
+  bool first = true;
+  while (n) {
+    if (n & 1) {
+      if (first) {
+        rh = bh;
+        rl = bl;
+        first = false;
+      } else {
+        dd_mul(rh, rl, bh, bl, rh, rl);
+      }
+    }
+    n >>= 1;
+    if (n) dd_mul(bh, bl, bh, bl, bh, bl);
+  }
+  return rh + rl;
+}
+
+// idm.py:17-31.  (s*/gap)**2 is the correctly rounded square, i.e. q*q.
+__device__ __forceinline__ double idm_accel(const Params& p, double v, double dv, double gap, double v_cap) {
+  double v0_eff = py_min(p.v0, v_cap);
+  double x = v / v0_eff;
+  double fr = p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
+  double inter;
+  if (isinf(gap)) {
+    inter = 0.0;
+  } else {
+    double s_star = p.s0 + py_max(0.0, v * p.T + v * dv / p.sqrt_ab2);
+    double q = s_star / gap;
+    inter = q * q;
+  }
+  return p.a_max * (1.0 - fr - inter);
+}
+
+// rng.py:24-41: splitmix64 finaliser fold over (seed, stream, id, step).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double keyed_uniform4(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  const uint64_t G = 0x9E3779B97F4A7C15ULL;
+  uint64_t h = mix64(0 + G + a);
+  h = mix64(h + G + b);
+  h = mix64(h + G + c);
+  h = mix64(h + G + d);
+  return (double)(h >> 11) * 0x1p-53;
+}
+
+// (s desc, vix asc): true if (sa, va) sorts before (sb, vb) in a lane.
+__device__ __forceinline__ bool ahead_of(double sa, int32_t va, double sb, int32_t vb) {
+  return sa > sb || (sa == sb && va < vb);
+}
+
+}  // namespace tsb

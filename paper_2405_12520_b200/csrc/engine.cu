@@ -1,0 +1,925 @@
+// engine.cu -- host side of the B200 engine: device memory, the per-step
+// launch sequence (captured once into a CUDA graph and replayed), host
+// continuation of reroutes, queries, and the C-ABI of include/tsb200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "router.h"
+
+#include "kernels.cu"  // single translation unit: kernels + host engine
+
+using namespace tsb;
+
+static thread_local std::string g_err;
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                           \
+  do {                                                                                                  \
+    cudaError_t _e = (x);                                                                               \
+    if (_e != cudaSuccess)                                                                              \
+      return fail(TSB_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(_e), __FILE__, __LINE__);        \
+  } while (0)
+#define RC(x)              \
+  do {                     \
+    int _r = (x);          \
+    if (_r) return _r;     \
+  } while (0)
+
+static const int SCAN_BT = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_BT * SCAN_IPT;
+
+enum KernelClass {
+  KC_UPDATE,
+  KC_SCAN,
+  KC_SCATTER,
+  KC_LANESORT_SWEEP,
+  KC_RESOLVE,
+  KC_SIGNALS,
+  KC_INJECT,
+  KC_REGROUP,
+  KC_SPEEDS,
+  KC_MISC,
+  KC_COUNT
+};
+static const char* kKernelNames[KC_COUNT] = {"k_update",  "k_scan",   "k_scatter", "k_lanesort_sweep", "k_resolve",
+                                             "k_signals", "k_inject", "k_regroup", "k_speeds",         "k_misc"};
+
+struct tsb_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Ctx c{};
+  Dyn* dyn_host = nullptr;  // pinned mirror of c.dyn
+  std::vector<void*> allocs;
+  // host copies (authoritative for control changes and host continuation)
+  int32_t n_lanes = 0, n_roads = 0, n_junc = 0, n_trips = 0;
+  std::vector<LaneRec> lanes;
+  std::vector<int32_t> succ, succ_dst_road;
+  std::vector<double> phase_dur;
+  std::vector<int32_t> junc_phase_off;
+  std::vector<uint64_t> green;
+  std::vector<uint8_t> junc_signal;
+  std::vector<VCold> cold;
+  std::vector<int32_t> dest;
+  std::unique_ptr<Router> router;
+  std::vector<std::vector<int32_t>> route_host;  // roads_seq per vix
+  int64_t pool_used = 0, pool_cap = 0;
+  int32_t n_closed = 0;
+  bool routes_stale = false;
+  bool graph_dirty = true;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int32_t launches_per_step = 0;
+  // profiling
+  bool profiling = false;
+  int n_ev = 0;
+  cudaEvent_t ev[2 * 96] = {};
+  int ev_class[96];
+};
+
+template <class T>
+static int dalloc(tsb_engine* e, T** p, size_t n) {
+  *p = nullptr;
+  cudaError_t er = cudaMalloc((void**)p, sizeof(T) * (n ? n : 1));
+  if (er != cudaSuccess) return fail(TSB_ECUDA, "cudaMalloc(%zu B): %s", sizeof(T) * n, cudaGetErrorString(er));
+  e->allocs.push_back((void*)*p);
+  cudaMemset(*p, 0, sizeof(T) * (n ? n : 1));
+  return TSB_OK;
+}
+template <class T>
+static int upload(tsb_engine* e, T** p, const T* src, size_t n) {
+  RC(dalloc(e, p, n));
+  if (n) CK(cudaMemcpy(*p, src, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return TSB_OK;
+}
+
+// ----------------------------------------------------------------- step issue
+
+static inline int grid_for(int64_t n, int block, int cap) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return (int)std::min<int64_t>(g, cap);
+}
+
+struct Launcher {
+  tsb_engine* e;
+  int count = 0;
+  void pre(int kc) {
+    if (e->profiling && e->n_ev < 96) {
+      e->ev_class[e->n_ev] = kc;
+      cudaEventRecord(e->ev[2 * e->n_ev], e->stream);
+    }
+  }
+  void post() {
+    if (e->profiling && e->n_ev < 96) {
+      cudaEventRecord(e->ev[2 * e->n_ev + 1], e->stream);
+      e->n_ev++;
+    }
+    count++;
+  }
+};
+
+#define LAUNCH(kc, kern, grid, block, ...)                  \
+  do {                                                      \
+    L.pre(kc);                                              \
+    kern<<<(grid), (block), 0, e->stream>>>(__VA_ARGS__);  \
+    L.post();                                               \
+  } while (0)
+
+static void scan(tsb_engine* e, Launcher& L, int kc, const int32_t* in, int32_t* out, int out_sel,
+                 const int32_t* n_dev, int32_t n_static, int64_t n_max, const int32_t* gate) {
+  Ctx& c = e->c;
+  cudaMemsetAsync(c.scan_status, 0, sizeof(unsigned long long) * c.scan_tiles_cap, e->stream);
+  cudaMemsetAsync(c.scan_tiles, 0, sizeof(int32_t), e->stream);
+  int grid = (int)(n_max / SCAN_TILE + 1);
+  LAUNCH(kc, (k_scan<SCAN_BT, SCAN_IPT>), grid, SCAN_BT, c, in, out, out_sel, n_dev, n_static, gate);
+}
+
+// phase 0 = whole step; 1 = through k_update; 2 = the rest (split mode).
+static void issue_step(tsb_engine* e, Launcher& L, int phase) {
+  Ctx& c = e->c;
+  Dyn* dy = c.dyn;
+  const int VB = 256;
+  const int vgrid = grid_for(e->n_trips, VB, 148 * 8);
+  const int wgrid = grid_for((int64_t)e->n_lanes * 32, VB, 148 * 32);
+  const int rgrid = grid_for((int64_t)e->n_roads * 32, VB, 148 * 16);
+  const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
+  const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
+  const int32_t NL = e->n_lanes;
+  if (phase != 2) {
+    LAUNCH(KC_MISC, k_begin_step, 1, 1, c);
+    cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->stream);
+    cudaMemsetAsync(c.cursor, 0, sizeof(int32_t) * NL, e->stream);
+    LAUNCH(KC_UPDATE, k_update, vgrid, VB, c);
+  }
+  if (phase == 1) return;
+  if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
+  // bucket the post-delta state by lane, sort each lane, tentative sweep
+  scan(e, L, KC_SCAN, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
+  LAUNCH(KC_MISC, k_set_nc, 1, 1, c);
+  LAUNCH(KC_SCATTER, k_scatter, vgrid, VB, c, SEL_B, &dy->n_a, nullptr, SEL_C, nullptr);
+  LAUNCH(KC_LANESORT_SWEEP, k_lanesort<true>, wgrid, VB, c, SEL_C, nullptr);
+  LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
+  if (c.p.controller == 1) {
+    cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->stream);
+    LAUNCH(KC_SIGNALS, k_lane_counts, vgrid, VB, c);
+  }
+  LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
+  LAUNCH(KC_MISC, k_clock, 1, 1, c);
+  // injection
+  cudaMemsetAsync(c.inj_cnt, 0, sizeof(int32_t) * NL, e->stream);
+  cudaMemsetAsync(c.inj_cursor, 0, sizeof(int32_t) * NL, e->stream);
+  LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
+  LAUNCH(KC_INJECT, k_inject_hist, vgrid, VB, c);
+  scan(e, L, KC_INJECT, c.inj_cnt, c.inj_start, SEL_NONE, nullptr, NL, NL, &dy->n_due);
+  LAUNCH(KC_INJECT, k_inject_scatter, vgrid, VB, c);
+  LAUNCH(KC_INJECT, k_inject_lanes, tgrid, VB, c);
+  LAUNCH(KC_INJECT, k_retry_flags, vgrid, VB, c);
+  scan(e, L, KC_INJECT, c.flag_in, c.flag_scan, SEL_NONE, &dy->n_due, 0, e->n_trips, &dy->n_due);
+  LAUNCH(KC_INJECT, k_retry_compact, vgrid, VB, c);
+  LAUNCH(KC_INJECT, k_inject_finish, 1, 1, c);
+  // next snapshot: full regroup only if membership / order changed
+  cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->stream);
+  cudaMemsetAsync(c.cursor, 0, sizeof(int32_t) * NL, e->stream);
+  LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->need_regroup);
+  scan(e, L, KC_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->need_regroup);
+  LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->need_regroup);
+  LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->need_regroup);
+  LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->need_regroup);
+  LAUNCH(KC_MISC, k_commit_layout, 1, 1, c);
+  LAUNCH(KC_SPEEDS, k_speeds, rgrid, VB, c);
+  LAUNCH(KC_MISC, k_end_step, 1, 1, c);
+}
+
+// ----------------------------------------------------------------- host side pieces
+
+static int sync_dyn(tsb_engine* e) {
+  CK(cudaMemcpyAsync(e->dyn_host, e->c.dyn, sizeof(Dyn), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (e->dyn_host->overflow)
+    return fail(TSB_ECAP, "engine capacity/consistency flag 0x%x set (speed windows or host-route state)",
+                e->dyn_host->overflow);
+  return TSB_OK;
+}
+
+static int ensure_pool(tsb_engine* e, int64_t need) {
+  if (e->pool_used + need <= e->pool_cap) return TSB_OK;
+  int64_t ncap = std::max<int64_t>(2 * e->pool_cap, e->pool_used + need + 1024);
+  int32_t* np_ = nullptr;
+  CK(cudaMalloc((void**)&np_, sizeof(int32_t) * ncap));
+  if (e->pool_used)
+    CK(cudaMemcpyAsync(np_, e->c.routes, sizeof(int32_t) * e->pool_used, cudaMemcpyDeviceToDevice, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  for (auto& p : e->allocs)
+    if (p == (void*)e->c.routes) {
+      cudaFree(p);
+      p = (void*)np_;
+    }
+  e->c.routes = np_;
+  e->pool_cap = ncap;
+  e->graph_dirty = true;
+  return TSB_OK;
+}
+
+// Append roads_seq for vix (host copy + device pool + cold record).
+static int set_route(tsb_engine* e, int32_t vix, const std::vector<int32_t>& roads, bool ok) {
+  VCold& cd = e->cold[vix];
+  if (!ok) {
+    cd.route_len = 0;
+    cd.route_off = 0;
+  } else {
+    RC(ensure_pool(e, (int64_t)roads.size()));
+    cd.route_off = e->pool_used;
+    cd.route_len = (int32_t)roads.size();
+    CK(cudaMemcpyAsync((int32_t*)e->c.routes + e->pool_used, roads.data(), sizeof(int32_t) * roads.size(),
+                       cudaMemcpyHostToDevice, e->stream));
+    e->pool_used += (int64_t)roads.size();
+  }
+  e->route_host[vix] = ok ? roads : std::vector<int32_t>();
+  CK(cudaMemcpyAsync((VCold*)e->c.cold + vix, &cd, sizeof(VCold), cudaMemcpyHostToDevice, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return TSB_OK;
+}
+
+// Routes for every trip whose route the reference would still compute at its
+// first injection attempt (never routed, still waiting), on the current
+// router state.  Called at create and after any control change.
+static int route_pending(tsb_engine* e, bool all) {
+  std::vector<uint8_t> routed(e->n_trips, 0), status(e->n_trips, 0);
+  if (!all && e->n_trips) {
+    CK(cudaMemcpy(routed.data(), e->c.routed, e->n_trips, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(status.data(), e->c.status, e->n_trips, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int32_t> idx, org, dst;
+  for (int32_t k = 0; k < e->n_trips; k++)
+    if (all || (!routed[k] && status[k] == TSB_STATUS_WAITING)) {
+      idx.push_back(k);
+      org.push_back(e->cold[k].origin_lane);
+      dst.push_back(e->dest[k]);
+    }
+  if (idx.empty()) return TSB_OK;
+  std::vector<std::vector<int32_t>> roads;
+  std::vector<uint8_t> ok;
+  e->router->route_batch(org, dst, roads, ok);
+  int64_t need = 0;
+  for (size_t q = 0; q < idx.size(); q++) need += ok[q] ? (int64_t)roads[q].size() : 0;
+  RC(ensure_pool(e, need));
+  std::vector<int32_t> flat;
+  flat.reserve(need);
+  for (size_t q = 0; q < idx.size(); q++) {
+    VCold& cd = e->cold[idx[q]];
+    if (ok[q]) {
+      cd.route_off = e->pool_used + (int64_t)flat.size();
+      cd.route_len = (int32_t)roads[q].size();
+      flat.insert(flat.end(), roads[q].begin(), roads[q].end());
+      e->route_host[idx[q]] = std::move(roads[q]);
+    } else {
+      cd.route_off = 0;
+      cd.route_len = 0;
+      e->route_host[idx[q]].clear();
+    }
+  }
+  if (!flat.empty())
+    CK(cudaMemcpy((int32_t*)e->c.routes + e->pool_used, flat.data(), sizeof(int32_t) * flat.size(),
+                  cudaMemcpyHostToDevice));
+  e->pool_used += (int64_t)flat.size();
+  CK(cudaMemcpy((VCold*)e->c.cold, e->cold.data(), sizeof(VCold) * e->n_trips, cudaMemcpyHostToDevice));
+  return TSB_OK;
+}
+
+static int host_conn_from(const tsb_engine* e, int32_t lane, int32_t road) {
+  const LaneRec& L = e->lanes[lane];
+  for (int k = 0; k < L.nsucc; k++)
+    if (e->succ_dst_road[L.succ_off + k] == road) return e->succ[L.succ_off + k];
+  return -1;
+}
+
+// Continuation of _apply_deltas (world.py:454-499) for vehicles that reached
+// a closed connector: host reroute (world.py:434-441) and the rest of the
+// transition loop, then write the vehicle back.
+static int host_continue(tsb_engine* e) {
+  Dyn& d = *e->dyn_host;
+  const int32_t nq = d.n_hostq;
+  if (nq == 0) return TSB_OK;
+  std::vector<int32_t> q(nq);
+  CK(cudaMemcpy(q.data(), e->c.hostq, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost));
+  std::vector<JuncState> sig(std::max(e->n_junc, 1));
+  if (e->n_junc) CK(cudaMemcpy(sig.data(), e->c.sig, sizeof(JuncState) * e->n_junc, cudaMemcpyDeviceToHost));
+  auto red = [&](int32_t conn) {
+    int32_t j = e->lanes[conn].junc;
+    if (!e->junc_signal[j]) return false;
+    return !((e->green[conn] >> sig[j].phase) & 1ULL);
+  };
+  const double new_time = d.time + e->c.p.dt;
+  int64_t fin_now = d.finished_now;
+  for (int32_t k = 0; k < nq; k++) {
+    const int32_t i = q[k];
+    VRec r;
+    CK(cudaMemcpy(&r, e->c.B + i, sizeof(VRec), cudaMemcpyDeviceToHost));
+    int32_t lane = r.lane, rp = r.rp, vix = r.vix;
+    double s = r.s, v = r.v;
+    bool arrived = false;
+    while (s > e->lanes[lane].len) {
+      const LaneRec& LT = e->lanes[lane];
+      std::vector<int32_t>& roads = e->route_host[vix];
+      if (LT.kind == TSB_KIND_ROAD) {
+        if (rp + 1 >= (int32_t)roads.size()) {
+          arrived = true;
+          break;
+        }
+        int32_t conn = host_conn_from(e, lane, roads[rp + 1]);
+        if (conn >= 0 && (!e->lanes[conn].open || !e->lanes[e->lanes[conn].succ1].open)) {
+          std::vector<int32_t> nr;
+          if (e->router->route(lane, e->dest[vix], nullptr, &nr, nullptr)) {
+            std::vector<int32_t> seq(roads.begin(), roads.begin() + rp);
+            seq.insert(seq.end(), nr.begin(), nr.end());
+            RC(set_route(e, vix, seq, true));
+            if (rp + 1 >= (int32_t)seq.size()) {
+              arrived = true;
+              break;
+            }
+            conn = host_conn_from(e, lane, seq[rp + 1]);
+          } else {
+            conn = -1;
+          }
+        }
+        if (conn < 0 || red(conn)) {
+          s = LT.len;
+          v = 0.0;
+          break;
+        }
+        s -= LT.len;
+        lane = conn;
+      } else {
+        s -= LT.len;
+        lane = LT.succ1;
+        rp += 1;
+      }
+    }
+    if (arrived) {
+      VRec snap;
+      CK(cudaMemcpy(&snap, e->c.lay[d.cur] + i, sizeof(VRec), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(e->c.fin_state + vix, &snap, sizeof(VRec), cudaMemcpyHostToDevice));
+      r.lane = -1;
+      uint8_t st = TSB_STATUS_FINISHED;
+      CK(cudaMemcpy(e->c.status + vix, &st, 1, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(e->c.finish + vix, &new_time, sizeof(double), cudaMemcpyHostToDevice));
+      FinEntry fe{vix, 0, d.step_no};
+      CK(cudaMemcpy(e->c.fin_log + d.fin_log_n + fin_now, &fe, sizeof(FinEntry), cudaMemcpyHostToDevice));
+      fin_now++;
+    } else {
+      r.lane = lane;
+      r.s = s;
+      r.v = v;
+      r.rp = rp;
+    }
+    CK(cudaMemcpy(e->c.B + i, &r, sizeof(VRec), cudaMemcpyHostToDevice));
+  }
+  d.finished_now = fin_now;
+  CK(cudaMemcpy(&e->c.dyn->finished_now, &fin_now, sizeof(int64_t), cudaMemcpyHostToDevice));
+  return TSB_OK;
+}
+
+static int ensure_windows(tsb_engine* e, int32_t n_steps) {
+  // highest window index reachable after n_steps more steps (host time mirror
+  // evolves exactly like the device: time += dt per step)
+  double t = e->dyn_host->time;
+  for (int32_t k = 0; k < n_steps; k++) t += e->c.p.dt;
+  int32_t need = (int32_t)(t / e->c.p.speed_window) + 1;
+  if (need <= e->c.n_win) return TSB_OK;
+  int32_t nw = std::max(need + 8, 2 * e->c.n_win);
+  double* ns;
+  long long* nc;
+  RC(dalloc(e, &ns, (size_t)e->n_roads * nw));
+  RC(dalloc(e, &nc, (size_t)e->n_roads * nw));
+  if (e->c.n_win > 0 && e->n_roads > 0) {
+    CK(cudaMemcpy2D(ns, sizeof(double) * nw, e->c.acc_sum, sizeof(double) * e->c.n_win, sizeof(double) * e->c.n_win,
+                    e->n_roads, cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy2D(nc, sizeof(long long) * nw, e->c.acc_cnt, sizeof(long long) * e->c.n_win,
+                    sizeof(long long) * e->c.n_win, e->n_roads, cudaMemcpyDeviceToDevice));
+  }
+  e->c.acc_sum = ns;
+  e->c.acc_cnt = nc;
+  e->c.n_win = nw;
+  e->graph_dirty = true;
+  return TSB_OK;
+}
+
+static int build_graph(tsb_engine* e) {
+  if (e->gexec) {
+    cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+  }
+  if (e->graph) {
+    cudaGraphDestroy(e->graph);
+    e->graph = nullptr;
+  }
+  CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+  Launcher L{e};
+  issue_step(e, L, 0);
+  CK(cudaStreamEndCapture(e->stream, &e->graph));
+  CK(cudaGraphInstantiate(&e->gexec, e->graph, 0));
+  e->launches_per_step = L.count;
+  e->graph_dirty = false;
+  return TSB_OK;
+}
+
+static int do_steps(tsb_engine* e, int32_t n) {
+  if (n <= 0) return TSB_OK;
+  RC(ensure_windows(e, n));
+  if (e->routes_stale) {
+    RC(route_pending(e, false));
+    e->routes_stale = false;
+  }
+  e->c.split = e->n_closed > 0 ? 1 : 0;
+  if (e->c.split || e->profiling) {
+    for (int32_t k = 0; k < n; k++) {
+      Launcher L{e};
+      if (e->c.split) {
+        issue_step(e, L, 1);
+        RC(sync_dyn(e));
+        RC(host_continue(e));
+        issue_step(e, L, 2);
+      } else {
+        issue_step(e, L, 0);
+      }
+      CK(cudaGetLastError());
+    }
+    return TSB_OK;
+  }
+  if (e->graph_dirty) RC(build_graph(e));
+  for (int32_t k = 0; k < n; k++) CK(cudaGraphLaunch(e->gexec, e->stream));
+  return TSB_OK;
+}
+
+// ================================================================= C-ABI
+
+extern "C" {
+
+const char* tsb_last_error(void) { return g_err.c_str(); }
+
+int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device, tsb_engine** out) {
+  if (!net || !tr || !p || !out) return fail(TSB_EINVAL, "null argument");
+  if (p->pow_mode != 0)
+    return fail(TSB_EINVAL, "pow_mode %d unsupported on device (0 = correctly rounded powers)", p->pow_mode);
+  auto e = std::make_unique<tsb_engine>();
+  e->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  const int32_t NL = e->n_lanes = net->n_lanes;
+  const int32_t NR = e->n_roads = net->n_roads;
+  const int32_t NJ = e->n_junc = net->n_junctions;
+  const int32_t N = e->n_trips = tr->n;
+  Ctx& c = e->c;
+  c.n_lanes = NL;
+  c.n_roads = NR;
+  c.n_junc = NJ;
+  c.n_trips = N;
+  Params& P = c.p;
+  P.dt = p->dt;
+  P.lookahead = p->lookahead;
+  P.v0 = p->idm_v0;
+  P.T = p->idm_T;
+  P.a_max = p->idm_a_max;
+  P.b = p->idm_b;
+  P.delta = p->idm_delta;
+  P.s0 = p->idm_s0;
+  P.politeness = p->mobil_politeness;
+  P.threshold = p->mobil_threshold;
+  P.b_safe = p->mobil_b_safe;
+  P.eval_prob = p->mobil_eval_prob;
+  P.L = p->vehicle_length;
+  P.speed_window = p->speed_window;
+  P.amber = p->amber;
+  P.s0_floor = p->s0_floor;
+  P.mp_interval = p->mp_interval;
+  P.mp_min_green = p->mp_min_green;
+  P.sqrt_ab2 = 2.0 * std::sqrt(p->idm_a_max * p->idm_b);
+  P.controller = p->controller;
+  P.delta_int = (p->idm_delta == std::floor(p->idm_delta) && p->idm_delta >= 1 && p->idm_delta <= 64)
+                    ? (int32_t)p->idm_delta
+                    : 0;
+  P.seed = p->seed;
+
+  // lanes
+  e->lanes.resize(NL);
+  e->succ.assign(net->succ, net->succ + net->succ_off[NL]);
+  e->succ_dst_road.resize(e->succ.size());
+  for (int32_t l = 0; l < NL; l++) {
+    LaneRec& r = e->lanes[l];
+    r.len = net->lane_len[l];
+    r.cap = net->lane_cap[l];
+    r.road = net->lane_road[l];
+    r.junc = net->lane_junction[l];
+    r.left = net->lane_left[l];
+    r.right = net->lane_right[l];
+    r.succ1 = net->lane_succ1[l];
+    r.pred1 = net->lane_pred1[l];
+    r.succ_off = net->succ_off[l];
+    int32_t ns = net->succ_off[l + 1] - net->succ_off[l];
+    if (ns > 32767) return fail(TSB_EINVAL, "lane %d has too many successors", l);
+    r.nsucc = (int16_t)ns;
+    r.kind = net->lane_kind[l];
+    r.open = net->lane_open[l];
+    if (!r.open && r.kind >= 0) e->n_closed++;
+  }
+  for (size_t k = 0; k < e->succ.size(); k++) {
+    int32_t cn = e->succ[k];
+    e->succ_dst_road[k] = (net->lane_kind[cn] == TSB_KIND_CONNECTOR) ? net->lane_road[net->lane_succ1[cn]] : -2;
+  }
+  e->phase_dur.assign(net->phase_dur, net->phase_dur + net->junc_phase_off[NJ]);
+  e->junc_phase_off.assign(net->junc_phase_off, net->junc_phase_off + NJ + 1);
+  e->green.assign(net->lane_green_mask, net->lane_green_mask + NL);
+  e->junc_signal.assign(net->junc_signal, net->junc_signal + NJ);
+  std::vector<int32_t> jc_off(NJ + 1, 0), jc;
+  for (int32_t l = 0; l < NL; l++)
+    if (net->lane_kind[l] == TSB_KIND_CONNECTOR) jc_off[net->lane_junction[l] + 1]++;
+  for (int32_t j = 0; j < NJ; j++) jc_off[j + 1] += jc_off[j];
+  jc.resize(jc_off[NJ]);
+  {
+    std::vector<int32_t> fill(jc_off.begin(), jc_off.end() - 1);
+    for (int32_t l = 0; l < NL; l++)
+      if (net->lane_kind[l] == TSB_KIND_CONNECTOR) jc[fill[net->lane_junction[l]]++] = l;
+  }
+  std::vector<JuncState> sig(NJ);
+  for (int32_t j = 0; j < NJ; j++) sig[j] = JuncState{net->junc_phase0[j], 0, net->junc_elapsed0[j], 0.0};
+
+  // trips
+  e->cold.resize(N);
+  e->dest.resize(N);
+  e->route_host.resize(N);
+  std::vector<int32_t> pend(N);
+  for (int32_t k = 0; k < N; k++) {
+    VCold& cd = e->cold[k];
+    cd.key = tr->key[k];
+    cd.route_off = 0;
+    cd.route_len = -1;
+    cd.origin_lane = tr->origin_lane[k];
+    cd.origin_s = tr->origin_s[k];
+    cd.depart = tr->departure[k];
+    e->dest[k] = tr->dest_lane[k];
+    pend[k] = k;
+  }
+  std::stable_sort(pend.begin(), pend.end(), [&](int32_t a, int32_t b) {
+    return tr->departure[a] < tr->departure[b];  // ties keep ascending id
+  });
+  std::vector<double> pend_dep(N);
+  for (int32_t k = 0; k < N; k++) pend_dep[k] = tr->departure[pend[k]];
+
+  e->router = std::make_unique<Router>(NL, net->lane_kind, net->lane_len, net->lane_cap, net->lane_open,
+                                       net->succ_off, net->succ, net->pred_off, net->pred, net->lane_road);
+
+  // device uploads
+  tsb_engine* E = e.get();
+  RC(upload(E, (LaneRec**)&c.lanes, e->lanes.data(), NL));
+  RC(upload(E, (int32_t**)&c.succ, e->succ.data(), e->succ.size()));
+  RC(upload(E, (int32_t**)&c.succ_dst_road, e->succ_dst_road.data(), e->succ_dst_road.size()));
+  RC(upload(E, (int32_t**)&c.road_lane_off, net->road_lane_off, NR + 1));
+  RC(upload(E, (int32_t**)&c.road_lanes, net->road_lanes, net->road_lane_off[NR]));
+  RC(upload(E, (int32_t**)&c.junc_phase_off, net->junc_phase_off, NJ + 1));
+  RC(upload(E, (double**)&c.phase_dur, net->phase_dur, net->junc_phase_off[NJ]));
+  RC(upload(E, (uint64_t**)&c.green, net->lane_green_mask, NL));
+  RC(upload(E, (uint8_t**)&c.junc_signal, net->junc_signal, NJ));
+  RC(upload(E, (int32_t**)&c.jc_off, jc_off.data(), NJ + 1));
+  RC(upload(E, (int32_t**)&c.jc, jc.data(), jc.size()));
+  RC(upload(E, &c.sig, sig.data(), NJ));
+  RC(upload(E, (VCold**)&c.cold, e->cold.data(), N));
+  RC(upload(E, (int32_t**)&c.pend_vix, pend.data(), N));
+  RC(upload(E, (double**)&c.pend_dep, pend_dep.data(), N));
+  RC(dalloc(E, &c.status, N));
+  RC(dalloc(E, &c.routed, N));
+  RC(dalloc(E, &c.finish, N));
+  RC(dalloc(E, &c.fin_state, N));
+  {
+    std::vector<double> nanv(N, std::nan(""));
+    if (N) CK(cudaMemcpy(c.finish, nanv.data(), sizeof(double) * N, cudaMemcpyHostToDevice));
+  }
+  for (int b = 0; b < 2; b++) {
+    RC(dalloc(E, &c.lay[b], N));
+    RC(dalloc(E, &c.start[b], (size_t)NL + 1));
+  }
+  RC(dalloc(E, &c.B, N));
+  RC(dalloc(E, &c.D, N));
+  RC(dalloc(E, &c.cnt, NL));
+  RC(dalloc(E, &c.cursor, NL));
+  c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, N) / SCAN_TILE + 2);
+  RC(dalloc(E, &c.scan_status, c.scan_tiles_cap));
+  RC(dalloc(E, &c.scan_tiles, 1));
+  RC(dalloc(E, &c.stage, (size_t)NL + 1));
+  RC(dalloc(E, &c.events, NL));
+  RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)N + 16));
+  RC(dalloc(E, &c.rs_inwork, NL));
+  RC(dalloc(E, &c.rs_touched, NL));
+  RC(dalloc(E, &c.rs_event, NL));
+  RC(dalloc(E, &c.rs_movedin, NL));
+  RC(dalloc(E, &c.rs_moved, N));
+  RC(dalloc(E, &c.rs_reverted, N));
+  RC(dalloc(E, &c.rs_members, N));
+  RC(dalloc(E, &c.rs_touched_list, (size_t)NL + N));
+  RC(dalloc(E, &c.retry, N));
+  RC(dalloc(E, &c.retry2, N));
+  RC(dalloc(E, &c.due, N));
+  RC(dalloc(E, &c.due_grp, N));
+  RC(dalloc(E, &c.inj_cnt, NL));
+  RC(dalloc(E, &c.inj_start, (size_t)NL + 1));
+  RC(dalloc(E, &c.inj_cursor, NL));
+  RC(dalloc(E, &c.outcome, N));
+  RC(dalloc(E, &c.flag_in, N));
+  RC(dalloc(E, &c.flag_scan, (size_t)N + 1));
+  RC(dalloc(E, &c.lane_counts, NL));
+  RC(dalloc(E, &c.fin_log, N));
+  RC(dalloc(E, &c.hostq, N));
+  RC(dalloc(E, &c.dyn, 1));
+  RC(dalloc(E, &c.scratch_d, 16));
+  CK(cudaMallocHost((void**)&e->dyn_host, sizeof(Dyn)));
+  for (int q = 0; q < 2 * 96; q++) CK(cudaEventCreate(&e->ev[q]));
+  memset(e->dyn_host, 0, sizeof(Dyn));
+  c.n_win = 0;
+  c.acc_sum = nullptr;
+  c.acc_cnt = nullptr;
+  // route pool + initial routes (computed with the construction-time router;
+  // recomputed for not-yet-routed trips after any control change)
+  e->pool_cap = 0;
+  e->pool_used = 0;
+  {
+    int32_t* p0;
+    RC(dalloc(E, &p0, 1024));
+    c.routes = p0;
+    e->pool_cap = 1024;
+  }
+  RC(route_pending(E, true));
+  RC(ensure_windows(E, 1));
+  CK(cudaDeviceSynchronize());
+  *out = e.release();
+  return TSB_OK;
+}
+
+void tsb_destroy(tsb_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  if (e->graph) cudaGraphDestroy(e->graph);
+  for (int q = 0; q < 2 * 96; q++)
+    if (e->ev[q]) cudaEventDestroy(e->ev[q]);
+  for (void* p : e->allocs) cudaFree(p);
+  if (e->dyn_host) cudaFreeHost(e->dyn_host);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+static void fill_report(const tsb_engine* e, tsb_report* r) {
+  const Dyn& d = *e->dyn_host;
+  r->time = d.time;
+  r->step_no = d.step_no;
+  r->driving = d.n_a;
+  r->waiting = (int64_t)(e->n_trips - d.pend_ptr) + d.n_retry;
+  r->finished = d.finished_total;
+  r->dropped = d.dropped;
+  r->injected_now = d.injected_now;
+  r->finished_now = d.finished_now;
+  r->vehicle_updates = d.vehicle_updates;
+  r->reverts_last = d.reverts_last;
+}
+
+int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  if (n_steps < 0) return fail(TSB_EINVAL, "steps must be non-negative");
+  CK(cudaSetDevice(e->device));
+  RC(do_steps(e, n_steps));
+  RC(sync_dyn(e));
+  if (last) fill_report(e, last);
+  return TSB_OK;
+}
+
+int tsb_report_get(tsb_engine* e, tsb_report* out) {
+  RC(sync_dyn(e));
+  fill_report(e, out);
+  return TSB_OK;
+}
+
+int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* vix, int32_t* lane, int32_t* road_pos,
+              double* s, double* v) {
+  RC(sync_dyn(e));
+  const Dyn& d = *e->dyn_host;
+  const int32_t n = d.n_a;
+  *n_driving = n;
+  if (lane_start) CK(cudaMemcpy(lane_start, e->c.start[d.cur], sizeof(int32_t) * (e->n_lanes + 1), cudaMemcpyDeviceToHost));
+  std::vector<VRec> buf(std::max(n, 1));
+  if (n) CK(cudaMemcpy(buf.data(), e->c.lay[d.cur], sizeof(VRec) * n, cudaMemcpyDeviceToHost));
+  for (int32_t k = 0; k < n; k++) {
+    if (vix) vix[k] = buf[k].vix;
+    if (lane) lane[k] = buf[k].lane;
+    if (road_pos) road_pos[k] = buf[k].rp;
+    if (s) s[k] = buf[k].s;
+    if (v) v[k] = buf[k].v;
+  }
+  return TSB_OK;
+}
+
+int tsb_status(tsb_engine* e, uint8_t* status, double* finish_time, int32_t* last_lane, double* last_s,
+               double* last_v, int32_t* last_rp) {
+  if (e->n_trips == 0) return TSB_OK;
+  if (status) CK(cudaMemcpy(status, e->c.status, e->n_trips, cudaMemcpyDeviceToHost));
+  if (finish_time) CK(cudaMemcpy(finish_time, e->c.finish, sizeof(double) * e->n_trips, cudaMemcpyDeviceToHost));
+  if (last_lane || last_s || last_v || last_rp) {
+    std::vector<VRec> fs(e->n_trips);
+    CK(cudaMemcpy(fs.data(), e->c.fin_state, sizeof(VRec) * e->n_trips, cudaMemcpyDeviceToHost));
+    for (int32_t k = 0; k < e->n_trips; k++) {
+      if (last_lane) last_lane[k] = fs[k].lane;
+      if (last_s) last_s[k] = fs[k].s;
+      if (last_v) last_v[k] = fs[k].v;
+      if (last_rp) last_rp[k] = fs[k].rp;
+    }
+  }
+  return TSB_OK;
+}
+
+int tsb_finished(tsb_engine* e, int64_t since, int64_t cap, int32_t* vix, double* finish_time, int64_t* n_out) {
+  RC(sync_dyn(e));
+  const int64_t total = e->dyn_host->fin_log_n;
+  int64_t n = std::max<int64_t>(0, std::min<int64_t>(total - since, cap));
+  *n_out = n;
+  if (n == 0) return TSB_OK;
+  std::vector<FinEntry> buf(n);
+  CK(cudaMemcpy(buf.data(), e->c.fin_log + since, sizeof(FinEntry) * n, cudaMemcpyDeviceToHost));
+  // reference order: by step, then by id (world.py:447 iterates sorted ids)
+  std::stable_sort(buf.begin(), buf.end(), [](const FinEntry& a, const FinEntry& b) {
+    return a.step != b.step ? a.step < b.step : a.vix < b.vix;
+  });
+  std::vector<double> fin(e->n_trips);
+  CK(cudaMemcpy(fin.data(), e->c.finish, sizeof(double) * e->n_trips, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < n; k++) {
+    vix[k] = buf[k].vix;
+    finish_time[k] = fin[buf[k].vix];
+  }
+  return TSB_OK;
+}
+
+int tsb_road_acc(tsb_engine* e, int32_t n_windows, double* sum, int64_t* count) {
+  RC(sync_dyn(e));
+  const int32_t W = e->c.n_win;
+  std::vector<double> s((size_t)e->n_roads * W);
+  std::vector<long long> c((size_t)e->n_roads * W);
+  if (!s.empty()) {
+    CK(cudaMemcpy(s.data(), e->c.acc_sum, sizeof(double) * s.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(c.data(), e->c.acc_cnt, sizeof(long long) * c.size(), cudaMemcpyDeviceToHost));
+  }
+  for (int32_t r = 0; r < e->n_roads; r++)
+    for (int32_t w = 0; w < n_windows; w++) {
+      bool in = w < W;
+      sum[(size_t)r * n_windows + w] = in ? s[(size_t)r * W + w] : 0.0;
+      count[(size_t)r * n_windows + w] = in ? c[(size_t)r * W + w] : 0;
+    }
+  return TSB_OK;
+}
+
+int tsb_min_front_gap(tsb_engine* e, double* out) {
+  k_min_gap<<<1, 1024, 0, e->stream>>>(e->c, e->c.scratch_d);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, e->c.scratch_d, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return TSB_OK;
+}
+
+int tsb_set_lane(tsb_engine* e, int32_t lane, double max_speed, int32_t open) {
+  if (lane < 0 || lane >= e->n_lanes || e->lanes[lane].kind < 0) return fail(TSB_ERANGE, "unknown lane %d", lane);
+  LaneRec& r = e->lanes[lane];
+  bool was_open = r.open;
+  r.cap = max_speed;
+  r.open = open ? 1 : 0;
+  e->n_closed += (was_open && !r.open) ? 1 : (!was_open && r.open) ? -1 : 0;
+  CK(cudaMemcpy((LaneRec*)e->c.lanes + lane, &r, sizeof(LaneRec), cudaMemcpyHostToDevice));
+  e->router->set_lane(lane, max_speed, open != 0);
+  e->routes_stale = true;  // router.rebuild(): routes not yet computed must use the new state
+  return TSB_OK;
+}
+
+int tsb_set_signal_phase(tsb_engine* e, int32_t j, int32_t phase) {
+  if (j < 0 || j >= e->n_junc || !e->junc_signal[j]) return fail(TSB_EINVAL, "junction %d is unsignalized", j);
+  int32_t np_ = e->junc_phase_off[j + 1] - e->junc_phase_off[j];
+  if (phase < 0 || phase >= np_)
+    return fail(TSB_ERANGE, "phase index %d out of range (program has %d phases)", phase, np_);
+  JuncState st{phase, 0, 0.0, 0.0};
+  CK(cudaMemcpy(e->c.sig + j, &st, sizeof(JuncState), cudaMemcpyHostToDevice));
+  return TSB_OK;
+}
+
+int tsb_signal_state(tsb_engine* e, int32_t* phase, double* elapsed) {
+  std::vector<JuncState> sig(std::max(e->n_junc, 1));
+  if (e->n_junc) CK(cudaMemcpy(sig.data(), e->c.sig, sizeof(JuncState) * e->n_junc, cudaMemcpyDeviceToHost));
+  for (int32_t j = 0; j < e->n_junc; j++) {
+    phase[j] = sig[j].phase;
+    elapsed[j] = sig[j].elapsed;
+  }
+  return TSB_OK;
+}
+
+int tsb_route(tsb_engine* e, int32_t origin, int32_t dest, int32_t cap, int32_t* lanes, int32_t* n, double* cost) {
+  std::vector<int32_t> path;
+  double c = -1.0;
+  *n = 0;
+  if (cost) *cost = -1.0;
+  if (!e->router->route(origin, dest, &path, nullptr, &c)) return TSB_OK;
+  if ((int32_t)path.size() > cap) return fail(TSB_ERANGE, "route longer than buffer (%zu)", path.size());
+  std::copy(path.begin(), path.end(), lanes);
+  *n = (int32_t)path.size();
+  if (cost) *cost = c;
+  return TSB_OK;
+}
+
+struct tsb_router {
+  std::unique_ptr<Router> r;
+};
+
+int tsb_router_create(const tsb_network* net, tsb_router** out) {
+  auto r = new tsb_router;
+  r->r = std::make_unique<Router>(net->n_lanes, net->lane_kind, net->lane_len, net->lane_cap, net->lane_open,
+                                  net->succ_off, net->succ, net->pred_off, net->pred, net->lane_road);
+  *out = r;
+  return TSB_OK;
+}
+void tsb_router_destroy(tsb_router* r) { delete r; }
+int tsb_router_route(tsb_router* r, int32_t origin, int32_t dest, int32_t cap, int32_t* lanes, int32_t* n,
+                     double* cost) {
+  std::vector<int32_t> path;
+  double c = -1.0;
+  *n = 0;
+  if (cost) *cost = -1.0;
+  if (!r->r->route(origin, dest, &path, nullptr, &c)) return TSB_OK;
+  if ((int32_t)path.size() > cap) return fail(TSB_ERANGE, "route longer than buffer (%zu)", path.size());
+  std::copy(path.begin(), path.end(), lanes);
+  *n = (int32_t)path.size();
+  if (cost) *cost = c;
+  return TSB_OK;
+}
+int tsb_router_reach(tsb_router* r, int32_t n_dests, const int32_t* dests, uint8_t* reach) {
+  std::vector<int32_t> d(dests, dests + n_dests);
+  r->r->reach(d, reach);
+  return TSB_OK;
+}
+
+int tsb_profile_steps(tsb_engine* e, int32_t n_steps, int32_t cap, double* kernel_ms) {
+  std::vector<double> acc(KC_COUNT, 0.0);
+  for (int32_t k = 0; k < n_steps; k++) {
+    RC(sync_dyn(e));
+    e->profiling = true;
+    e->n_ev = 0;
+    int rc = do_steps(e, 1);
+    e->profiling = false;
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    for (int q = 0; q < e->n_ev; q++) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e->ev[2 * q], e->ev[2 * q + 1]));
+      acc[e->ev_class[q]] += ms;
+    }
+  }
+  for (int k = 0; k < KC_COUNT && k < cap; k++) kernel_ms[k] = n_steps ? acc[k] / n_steps : 0.0;
+  RC(sync_dyn(e));
+  return KC_COUNT;
+}
+
+const char* tsb_kernel_name(int32_t k) { return (k >= 0 && k < KC_COUNT) ? kKernelNames[k] : ""; }
+
+int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  RC(ensure_windows(e, n_steps));
+  if (e->graph_dirty && !e->c.split) RC(build_graph(e));
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaEventRecord(a, e->stream));
+  RC(do_steps(e, n_steps));
+  CK(cudaEventRecord(b, e->stream));
+  CK(cudaEventSynchronize(b));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, a, b));
+  *ms = f;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  RC(sync_dyn(e));
+  return TSB_OK;
+}
+
+int tsb_launches_per_step(tsb_engine* e, int32_t* n) {
+  if (e->graph_dirty) RC(build_graph(e));
+  *n = e->launches_per_step;
+  return TSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1074 @@
+// kernels.cu -- the per-step device pipeline of the MOSS vehicle loop.
+//
+// One step (World.step, trafficsim/engine/world.py:659-689) is the sequence
+//
+//   k_update    A -> B     prepare-consumer + update + lane/road transitions
+//                          (world.py:261-419, 443-499), fused lane histogram
+//   k_scan      cnt -> C_start
+//   k_scatter   B -> D     bucket by post-delta lane
+//   k_lanesort  D -> C     per-lane sort by (s desc, id asc) + tentative
+//                          collision sweep (world.py:509-559)
+//   k_resolve   C          exact revert chains (rare, single thread)
+//   k_signals              world.py:619-647, time += dt, step_no++
+//   k_inject_*             world.py:561-617, per origin lane
+//   k_regroup_* C -> A'    only when membership/order changed
+//   k_speeds               world.py:649-657
+//
+// The snapshot layout A is the reference's per-lane index itself
+// (world.py:227-242): vehicles grouped by lane, s descending, id ascending,
+// so "leader" is the previous record and the MOBIL / sensing lookups are
+// binary searches in a contiguous segment.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "device.cuh"
+
+namespace tsb {
+
+enum { GREEN = 0, AMBER = 1, RED = 2 };
+enum : uint8_t { OUT_NONE = 0, OUT_INJECT = 1, OUT_RETRY = 2, OUT_DROP = 3 };
+
+static constexpr double EPS_GAP = 1e-6;  // world.py:43
+
+__device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
+
+// Buffer selectors: the snapshot layout A and the post-sweep layout C swap
+// roles through dyn->cur (a device value), so kernels captured once in a
+// CUDA graph pick their buffers at run time.
+enum { SEL_A = 0, SEL_C = 1, SEL_B = 2, SEL_D = 3, SEL_NONE = 4 };
+__device__ __forceinline__ VRec* rec_buf(const Ctx& c, int sel) {
+  const int cur = c.dyn->cur;
+  switch (sel) {
+    case SEL_A: return c.lay[cur];
+    case SEL_C: return c.lay[cur ^ 1];
+    case SEL_B: return c.B;
+    default: return c.D;
+  }
+}
+__device__ __forceinline__ int32_t* start_buf(const Ctx& c, int sel) {
+  return sel == SEL_A ? c.start[c.dyn->cur] : c.start[c.dyn->cur ^ 1];
+}
+__device__ __forceinline__ bool gated_off(const int32_t* gate) { return gate && *gate == 0; }
+
+// ------------------------------------------------------------------ network helpers
+
+// _conn_from[(lane, road)] (world.py:155-166): smallest successor connector
+// of road lane `lane` leading onto `road`.  Successor lists are sorted.
+__device__ __forceinline__ int32_t conn_from(const Ctx& c, const LaneRec& L, int32_t road) {
+  for (int k = 0; k < L.nsucc; k++)
+    if (c.succ_dst_road[L.succ_off + k] == road) return c.succ[L.succ_off + k];
+  return -1;
+}
+
+// world.py:247-254 + signals.py:46-61
+__device__ __forceinline__ int aspect(const Ctx& c, int32_t conn) {
+  int32_t j = c.lanes[conn].junc;
+  if (!c.junc_signal[j]) return GREEN;
+  JuncState st = c.sig[j];
+  if (!((c.green[conn] >> st.phase) & 1ULL)) return RED;
+  double dur = c.phase_dur[c.junc_phase_off[j] + st.phase];
+  if (c.p.controller == 0 && c.p.amber > 0.0 && st.elapsed >= dur - c.p.amber) return AMBER;
+  return GREEN;
+}
+
+struct View {
+  bool ok;
+  double s, v;
+};
+
+__device__ __forceinline__ View view_at(const VRec* A, int32_t k) {
+  if (k < 0) return View{false, 0.0, 0.0};
+  return View{true, A[k].s, A[k].v};
+}
+
+// ------------------------------------------------------------------ MOBIL (mobil.py:33-98)
+
+__device__ __forceinline__ double gap_to(const View& l, double fs, double Lv) {
+  return l.ok ? l.s - Lv - fs : CUDART_INF;
+}
+__device__ __forceinline__ double accel_behind(const Params& p, double me_v, const View& l, double gap, double cap) {
+  double dv = me_v - (l.ok ? l.v : 0.0);
+  return idm_accel(p, me_v, dv, gap, cap);
+}
+
+__device__ bool evaluate_change(const Params& p, View me, View cl, View cf, View tl, View tf, double s_t,
+                                double cap_cur, double cap_tgt, double& incentive) {
+  const double Lv = p.L;
+  double g_tl = gap_to(tl, s_t, Lv);
+  double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
+  if (g_tl <= 0.0 || g_tf <= 0.0) return false;
+  double g_cur = gap_to(cl, me.s, Lv);
+  double a_me = (g_cur <= 0.0) ? -CUDART_INF : accel_behind(p, me.v, cl, g_cur, cap_cur);
+  double a_me_new = accel_behind(p, me.v, tl, g_tl, cap_tgt);
+  double a_nf = 0.0, a_nf_new = 0.0;
+  if (tf.ok) {
+    double g_nf_old = gap_to(tl, tf.s, Lv);
+    if (g_nf_old <= 0.0) return false;
+    a_nf = accel_behind(p, tf.v, tl, g_nf_old, cap_tgt);
+    View mev{true, s_t, me.v};
+    a_nf_new = accel_behind(p, tf.v, mev, g_tf, cap_tgt);
+    if (a_nf_new < -p.b_safe) return false;
+  }
+  double a_of = 0.0, a_of_new = 0.0;
+  if (cf.ok) {
+    double g_of_old = me.s - Lv - cf.s;
+    double g_of_new = gap_to(cl, cf.s, Lv);
+    if (g_of_old > 0.0 && g_of_new > 0.0) {
+      a_of = accel_behind(p, cf.v, me, g_of_old, cap_cur);
+      a_of_new = accel_behind(p, cf.v, cl, g_of_new, cap_cur);
+    }
+  }
+  if (a_me == -CUDART_INF)
+    incentive = CUDART_INF;
+  else
+    incentive = (a_me_new - a_me) + p.politeness * ((a_nf_new - a_nf) + (a_of_new - a_of));
+  return true;
+}
+
+// Number of records in A[lo, hi) strictly above s_t (world.py:325-330):
+// leader = lo+m-1, follower = lo+m.
+__device__ __forceinline__ int32_t count_above(const VRec* A, int32_t lo, int32_t hi, double s_t) {
+  int32_t a = lo, b = hi;
+  while (a < b) {
+    int32_t m = (a + b) >> 1;
+    if (A[m].s > s_t)
+      a = m + 1;
+    else
+      b = m;
+  }
+  return a - lo;
+}
+
+// Records ahead of (s, vix) in (s desc, id asc) order (world.py:276-280).
+__device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_t hi, double s, int32_t vix) {
+  int32_t a = lo, b = hi;
+  while (a < b) {
+    int32_t m = (a + b) >> 1;
+    if (ahead_of(A[m].s, A[m].vix, s, vix))
+      a = m + 1;
+    else
+      b = m;
+  }
+  return a - lo;
+}
+
+// ------------------------------------------------------------------ k_update
+
+// World._update_vehicle + World._apply_deltas for one vehicle.
+__global__ void k_update(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t n = dy->n_a;
+  const VRec* A = c.lay[dy->cur];
+  const int32_t* S = c.start[dy->cur];
+  const Params& p = c.p;
+  const uint64_t step_no = (uint64_t)dy->step_no;
+  const double new_time = dy->time + p.dt;
+  for (int32_t i = gtid(); i < n; i += gstride()) {
+    const VRec me = A[i];
+    const int32_t snap_lane = me.lane;
+    const LaneRec L0 = c.lanes[snap_lane];
+    const int32_t lo0 = S[snap_lane], hi0 = S[snap_lane + 1], pos = i - lo0;
+    const VCold cd = c.cold[me.vix];
+    const int32_t* roads = c.routes + cd.route_off;
+    const int32_t nroads = cd.route_len;
+    const int32_t rp = me.rp;
+
+    // ---- _consider_change (world.py:344-397)
+    int32_t lane = snap_lane;
+    double s = me.s;
+    const double v = me.v;
+    bool changed = false;
+    if (L0.kind == TSB_KIND_ROAD && (L0.left >= 0 || L0.right >= 0)) {
+      const bool any = rp + 1 >= nroads;
+      const int32_t nr = any ? -1 : roads[rp + 1];
+      const bool mandatory = !any && conn_from(c, L0, nr) < 0;
+      bool go = true;
+      int32_t sides[2] = {L0.left, L0.right};
+      int nsides = 2;
+      if (mandatory) {
+        int32_t below = -1, above = -1;
+        for (int32_t k = c.road_lane_off[L0.road]; k < c.road_lane_off[L0.road + 1]; k++) {
+          int32_t f = c.road_lanes[k];
+          if (conn_from(c, c.lanes[f], nr) < 0) continue;
+          if (f < lane && (below < 0 || f > below)) below = f;
+          if (f > lane && (above < 0 || f < above)) above = f;
+        }
+        double dl = below >= 0 ? (double)(lane - below) : CUDART_INF;
+        double dr = above >= 0 ? (double)(above - lane) : CUDART_INF;
+        sides[0] = dl <= dr ? L0.left : L0.right;
+        nsides = 1;
+      } else {
+        double draw = keyed_uniform4(p.seed, 1ULL, cd.key, step_no);
+        go = !(draw >= p.eval_prob);
+      }
+      if (go) {
+        View mev{true, me.s, v};
+        View cl = view_at(A, pos > 0 ? i - 1 : -1);
+        View cf = view_at(A, i + 1 < hi0 ? i + 1 : -1);
+        bool have = false;
+        double best_inc = 0.0, best_s = 0.0;
+        int32_t best_nb = -1;
+        for (int k = 0; k < nsides; k++) {
+          int32_t nb = sides[k];
+          if (nb < 0) continue;
+          const LaneRec LN = c.lanes[nb];
+          if (!LN.open) continue;
+          if (!mandatory && !any && conn_from(c, LN, nr) < 0) continue;
+          double s_t = me.s * (LN.len / L0.len);
+          int32_t lo = S[nb], hi = S[nb + 1];
+          int32_t m = count_above(A, lo, hi, s_t);
+          View tl = view_at(A, m > 0 ? lo + m - 1 : -1);
+          View tf = view_at(A, lo + m < hi ? lo + m : -1);
+          double inc;
+          if (!evaluate_change(p, mev, cl, cf, tl, tf, s_t, L0.cap, LN.cap, inc)) continue;
+          if (!mandatory && inc <= p.threshold) continue;
+          if (!have || inc > best_inc || (inc == best_inc && nb < best_nb)) {
+            have = true;
+            best_inc = inc;
+            best_nb = nb;
+            best_s = s_t;
+          }
+        }
+        if (have) {
+          changed = true;
+          lane = best_nb;
+          s = best_s;
+        }
+      }
+    }
+
+    // ---- _sense (world.py:261-317)
+    const LaneRec L1 = changed ? c.lanes[lane] : L0;
+    double gap = CUDART_INF, lead_v = 0.0;
+    bool found = false;
+    {
+      int32_t lo = S[lane], hi = S[lane + 1];
+      if (hi > lo) {
+        int32_t ld = -1;
+        if (!changed) {
+          if (pos > 0) ld = i - 1;
+        } else {
+          int32_t m = count_ahead(A, lo, hi, s, me.vix);
+          if (m > 0) ld = lo + m - 1;
+        }
+        if (ld >= 0) {
+          gap = py_max(A[ld].s - p.L - s, EPS_GAP);
+          lead_v = A[ld].v;
+          found = true;
+        }
+      }
+    }
+    if (!found) {
+      const double remaining = L1.len - s;
+      bool stop = false;
+      if (L1.kind == TSB_KIND_ROAD) {
+        if (rp + 1 >= nroads) {
+          gap = CUDART_INF;
+          lead_v = 0.0;
+          found = true;
+        } else {
+          int32_t conn = conn_from(c, L1, roads[rp + 1]);
+          if (conn < 0 || !c.lanes[conn].open || !c.lanes[c.lanes[conn].succ1].open) {
+            stop = true;
+          } else {
+            int asp = aspect(c, conn);
+            if (asp == RED || (asp == AMBER && remaining > v * v / (2.0 * p.b))) stop = true;
+          }
+        }
+        if (stop) {
+          gap = py_max(remaining, EPS_GAP);
+          lead_v = 0.0;
+          found = true;
+        }
+      }
+      if (!found) {
+        int32_t cur = lane, cur_rp = rp;
+        LaneRec LC = L1;
+        double dist = remaining;
+        gap = CUDART_INF;
+        lead_v = 0.0;
+        while (dist < p.lookahead) {
+          int32_t nxt;
+          if (LC.kind == TSB_KIND_ROAD) {
+            nxt = (cur_rp + 1 >= nroads) ? -1 : conn_from(c, LC, roads[cur_rp + 1]);
+            if (nxt < 0 || !c.lanes[nxt].open) break;
+          } else {
+            nxt = LC.succ1;
+            cur_rp += 1;
+            if (!c.lanes[nxt].open) break;
+          }
+          int32_t lo = S[nxt], hi = S[nxt + 1];
+          if (hi > lo) {
+            const VRec rear = A[hi - 1];
+            double g = dist + rear.s - p.L;
+            gap = py_max(g, EPS_GAP);
+            lead_v = rear.v;
+            break;
+          }
+          LC = c.lanes[nxt];
+          dist += LC.len;
+          cur = nxt;
+        }
+        (void)cur;
+      }
+    }
+
+    // ---- IDM + integration (world.py:406-419)
+    const double a = idm_accel(p, v, v - lead_v, gap, L1.cap);
+    const double dt = p.dt;
+    double v_new = v + a * dt, disp;
+    if (v_new <= 0.0) {
+      v_new = 0.0;
+      disp = a < 0.0 ? v * v / (2.0 * -a) : 0.0;
+    } else {
+      disp = v * dt + 0.5 * a * dt * dt;
+      if (disp < 0.0) disp = 0.0;
+    }
+    double ns = s + disp, nv = v_new;
+    int32_t nl = lane, nrp = rp;
+
+    // ---- _apply_deltas transitions (world.py:443-499)
+    LaneRec LT = L1;
+    bool arrived = false, host = false;
+    while (ns > LT.len) {
+      if (LT.kind == TSB_KIND_ROAD) {
+        if (nrp + 1 >= nroads) {
+          arrived = true;
+          break;
+        }
+        int32_t conn = conn_from(c, LT, roads[nrp + 1]);
+        if (conn >= 0 && (!c.lanes[conn].open || !c.lanes[c.lanes[conn].succ1].open)) {
+          host = true;  // reroute needs the host router (world.py:460-469)
+          break;
+        }
+        if (conn < 0 || aspect(c, conn) == RED) {
+          ns = LT.len;
+          nv = 0.0;
+          break;
+        }
+        ns -= LT.len;
+        nl = conn;
+        LT = c.lanes[conn];
+      } else {
+        ns -= LT.len;
+        nl = LT.succ1;
+        nrp += 1;
+        LT = c.lanes[nl];
+      }
+    }
+    VRec out{ns, nv, me.vix, nrp, nl, i};
+    if (arrived) {
+      out.lane = -1;
+      c.status[me.vix] = TSB_STATUS_FINISHED;
+      c.finish[me.vix] = new_time;
+      c.fin_state[me.vix] = me;
+      unsigned long long k = atomicAdd((unsigned long long*)&dy->finished_now, 1ULL);
+      FinEntry fe;
+      fe.vix = me.vix;
+      fe.pad = 0;
+      fe.step = (int64_t)step_no;
+      c.fin_log[dy->fin_log_n + (int64_t)k] = fe;
+    } else if (host) {
+      int32_t k = atomicAdd(&dy->n_hostq, 1);
+      c.hostq[k] = i;
+      if (!c.split) {  // closures only occur in split mode; keep the state consistent
+        out.lane = nl;
+        atomicAdd(&c.cnt[nl], 1);
+      }
+    } else {
+      atomicAdd(&c.cnt[nl], 1);
+    }
+    c.B[i] = out;
+  }
+}
+
+// Fix-up after host continuation of rerouted vehicles: count their lanes.
+__global__ void k_count_hostq(Ctx c) {
+  Dyn* dy = c.dyn;
+  for (int32_t k = gtid(); k < dy->n_hostq; k += gstride()) {
+    const VRec r = c.B[c.hostq[k]];
+    if (r.lane >= 0) atomicAdd(&c.cnt[r.lane], 1);
+  }
+}
+
+// ------------------------------------------------------------------ scan
+
+// Exclusive scan of in[0, n) into out[0, n] (out[n] = total), single pass
+// with decoupled look-back.  status[] and *tiles must be zero on entry.
+// n is read from *n_dev when n_dev != nullptr.
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) k_scan(Ctx c, const int32_t* in, int32_t* out, int out_sel, const int32_t* n_dev,
+                                             int32_t n_static, const int32_t* gate) {
+  if (gated_off(gate)) return;
+  if (out_sel != SEL_NONE) out = start_buf(c, out_sel);
+  unsigned long long* status = c.scan_status;
+  int32_t* tiles = c.scan_tiles;
+  const int32_t n = n_dev ? *n_dev : n_static;
+  __shared__ int32_t s_tile, s_prefix;
+  __shared__ int32_t s_warp[BT / 32];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tiles, 1);
+  __syncthreads();
+  const int32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * BT * IPT;
+  if (base > n) return;
+  int32_t v[IPT];
+  int32_t local = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; k++) {
+    int64_t idx = base + (int64_t)threadIdx.x * IPT + k;
+    v[k] = idx < n ? in[idx] : 0;
+    local += v[k];
+  }
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < BT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < BT / 32) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const int32_t warp_excl = warp ? s_warp[warp - 1] : 0;
+  const int32_t total = s_warp[BT / 32 - 1];
+  int32_t excl = warp_excl + x - local;
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* st = status;
+    if (tile == 0) {
+      __threadfence();
+      st[0] = (2ULL << 32) | (unsigned)total;
+      s_prefix = 0;
+    } else {
+      st[tile] = (1ULL << 32) | (unsigned)total;
+      __threadfence();
+      int32_t acc = 0;
+      int32_t t = tile - 1;
+      for (;;) {
+        unsigned long long w = st[t];
+        unsigned flag = (unsigned)(w >> 32);
+        if (flag == 0) continue;
+        acc += (int32_t)(unsigned)(w & 0xffffffffULL);
+        if (flag == 2) break;
+        t--;
+      }
+      __threadfence();
+      st[tile] = (2ULL << 32) | (unsigned)(acc + total);
+      s_prefix = acc;
+    }
+  }
+  __syncthreads();
+  int32_t run = s_prefix + excl;
+#pragma unroll
+  for (int k = 0; k < IPT; k++) {
+    int64_t idx = base + (int64_t)threadIdx.x * IPT + k;
+    if (idx <= n) out[idx] = run;
+    run += v[k];
+  }
+}
+
+// ------------------------------------------------------------------ scatter / sort / sweep
+
+// Bucket records by lane: dst[start[lane] + cursor++].  Records with lane < 0
+// (arrivals) are dropped.  src has *n_ptr (+ *n_extra) records.
+__global__ void k_scatter(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* n_extra, int start_sel,
+                          const int32_t* gate) {
+  if (gated_off(gate)) return;
+  const VRec* src = rec_buf(c, src_sel);
+  const int32_t* start = start_buf(c, start_sel);
+  VRec* dst = c.D;
+  const int32_t n = *n_ptr + (n_extra ? *n_extra : 0);
+  for (int32_t i = gtid(); i < n; i += gstride()) {
+    const VRec r = src[i];
+    if (r.lane < 0) continue;
+    int32_t k = atomicAdd(&c.cursor[r.lane], 1);
+    dst[start[r.lane] + k] = r;
+  }
+}
+
+__global__ void k_hist(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* n_extra, const int32_t* gate) {
+  if (gated_off(gate)) return;
+  const VRec* src = rec_buf(c, src_sel);
+  const int32_t n = *n_ptr + (n_extra ? *n_extra : 0);
+  for (int32_t i = gtid(); i < n; i += gstride()) {
+    int32_t l = src[i].lane;
+    if (l >= 0) atomicAdd(&c.cnt[l], 1);
+  }
+}
+
+// Warp per lane: sort D[lo,hi) by (s desc, vix asc) into C[lo,hi), then (if
+// sweep) the tentative collision sweep of world.py:524-555 on this lane from
+// its post-delta state.  A lane whose sweep would revert a vehicle is left
+// unswept (C keeps the sorted post-delta values) and queued for k_resolve.
+template <bool SWEEP>
+__global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
+  if (gated_off(gate)) return;
+  const VRec* D = c.D;
+  VRec* C = rec_buf(c, dst_sel);
+  const int32_t* start = start_buf(c, dst_sel);
+  const VRec* snapA = rec_buf(c, SEL_A);
+  const int lane_id = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const Params& p = c.p;
+  Dyn* dy = c.dyn;
+  for (int32_t L = gtid() >> 5; L < c.n_lanes; L += warps) {
+    const int32_t lo = start[L], hi = start[L + 1], n = hi - lo;
+    if (n == 0) continue;
+    // rank sort (keys unique: vix distinct)
+    for (int32_t j = lane_id; j < n; j += 32) {
+      const VRec r = D[lo + j];
+      int32_t rank = 0;
+      for (int32_t k = 0; k < n; k++) {
+        const double sk = D[lo + k].s;
+        const int32_t vk = D[lo + k].vix;
+        rank += ahead_of(sk, vk, r.s, r.vix) ? 1 : 0;
+      }
+      C[lo + rank] = r;
+    }
+    __syncwarp();
+    if (!SWEEP) continue;
+    // parallel trigger test on unclamped predecessors
+    int32_t first = n;
+    for (int32_t j = lane_id; j < n; j += 32) {
+      if (j == 0) continue;
+      double limit = (C[lo + j - 1].s - p.L) - p.s0_floor;
+      if (C[lo + j].s > limit + 1e-12) first = min(first, j);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if (first >= n) continue;
+    if (lane_id == 0) {
+      // sequential sweep from `first` (everything before is untouched)
+      VRec prev = C[lo + first - 1];
+      bool prev_entered = prev.lane != snapA[prev.src].lane;
+      double prev_rear = prev.s - p.L;
+      bool event = false;
+      int32_t k = first;
+      for (; k < n; k++) {
+        VRec r = C[lo + k];
+        const double limit = prev_rear - p.s0_floor;
+        const VRec sn = snapA[r.src];
+        const bool entered = r.lane != sn.lane;
+        if (r.s > limit + 1e-12) {
+          const double floor_s = entered ? 0.0 : sn.s;
+          if (limit >= floor_s) {
+            r.v = py_max(0.0, py_min(r.v, r.v - (r.s - limit) / p.dt));
+            r.s = limit;
+          } else if (entered) {  // not reverted: no vehicle is reverted before resolve
+            event = true;
+            break;
+          } else if (prev_entered) {
+            event = true;
+            break;
+          } else {
+            r.v = 0.0;
+            r.s = floor_s;
+          }
+          C[lo + k].s = r.s;
+          C[lo + k].v = r.v;
+        }
+        prev_entered = entered;
+        prev_rear = r.s - p.L;
+      }
+      if (event) {
+        // restore the post-delta values written so far; resolve re-sweeps
+        for (int32_t q = first; q < k; q++) {
+          const VRec o = c.B[C[lo + q].src];
+          C[lo + q].s = o.s;
+          C[lo + q].v = o.v;
+        }
+        int32_t e = atomicAdd(&dy->n_events, 1);
+        c.events[e] = L;
+      } else {
+        // a hold can break the (s desc) order; the next snapshot must be re-sorted
+        for (int32_t q = (first > 0 ? first - 1 : 0); q + 1 < n; q++)
+          if (!ahead_of(C[lo + q].s, C[lo + q].vix, C[lo + q + 1].s, C[lo + q + 1].vix)) {
+            dy->need_regroup = 1;
+            break;
+          }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ resolve (exact revert chains)
+
+// Min-heap of lane ids in global scratch.
+__device__ void heap_push(int32_t* h, int32_t& n, int32_t x) {
+  int32_t i = n++;
+  h[i] = x;
+  while (i > 0) {
+    int32_t pa = (i - 1) >> 1;
+    if (h[pa] <= h[i]) break;
+    int32_t t = h[pa];
+    h[pa] = h[i];
+    h[i] = t;
+    i = pa;
+  }
+}
+__device__ int32_t heap_pop(int32_t* h, int32_t& n) {
+  int32_t top = h[0];
+  h[0] = h[--n];
+  int32_t i = 0;
+  for (;;) {
+    int32_t a = 2 * i + 1, b = a + 1, m = i;
+    if (a < n && h[a] < h[m]) m = a;
+    if (b < n && h[b] < h[m]) m = b;
+    if (m == i) break;
+    int32_t t = h[m];
+    h[m] = h[i];
+    h[i] = t;
+    i = m;
+  }
+  return top;
+}
+
+// Replays the reference's restart-after-revert sweep exactly, touching only
+// lanes involved in revert chains.  Lanes are
+// processed in the order the reference would next sweep them "for real":
+// always the smallest pending lane.  A lane that the reference has not yet
+// swept when it receives a reverted vehicle (id > reach) is first restored
+// to its post-delta state, because k_lanesort already applied its
+// tentative (membership-stale) sweep.
+__global__ void k_resolve(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t ne = dy->n_events;
+  if (ne == 0 || threadIdx.x != 0 || blockIdx.x != 0) return;
+  const Params& p = c.p;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  int32_t* heap = c.rs_heap;
+  int32_t hn = 0, nt = 0, nmoved = 0;
+  for (int32_t e = 0; e < ne; e++) {
+    int32_t L = c.events[e];
+    c.rs_event[L] = 1;
+    c.rs_inwork[L] = 1;
+    heap_push(heap, hn, L);
+  }
+  int32_t reach = -1;
+  int64_t reverts = 0;
+  const int64_t max_reverts = (int64_t)dy->n_c + 2;
+  while (hn > 0) {
+    const int32_t L = heap_pop(heap, hn);
+    if (!c.rs_inwork[L]) continue;
+    c.rs_inwork[L] = 0;
+    if (!c.rs_touched[L]) {
+      c.rs_touched[L] = 1;
+      c.rs_touched_list[nt++] = L;
+    }
+    if (L > reach) reach = L;
+    // members: segment entries still on L, plus vehicles reverted into L
+    int32_t m = 0;
+    for (int32_t j = CS[L]; j < CS[L + 1]; j++)
+      if (C[j].lane == L) c.rs_members[m++] = j;
+    if (c.rs_movedin[L])
+      for (int32_t q = 0; q < nmoved; q++) {
+        int32_t j = c.rs_moved[q];
+        if (C[j].lane == L && (j < CS[L] || j >= CS[L + 1])) c.rs_members[m++] = j;
+      }
+    // insertion sort by (s desc, vix asc)
+    for (int32_t a = 1; a < m; a++) {
+      int32_t x = c.rs_members[a];
+      int32_t b = a - 1;
+      while (b >= 0 && ahead_of(C[x].s, C[x].vix, C[c.rs_members[b]].s, C[c.rs_members[b]].vix)) {
+        c.rs_members[b + 1] = c.rs_members[b];
+        b--;
+      }
+      c.rs_members[b + 1] = x;
+    }
+    // the reference's sweep of this lane (world.py:527-555)
+    int32_t prev = -1;
+    double prev_rear = CUDART_INF;
+    int32_t rev = -1;
+    for (int32_t a = 0; a < m; a++) {
+      const int32_t j = c.rs_members[a];
+      VRec& r = C[j];
+      const double limit = prev_rear - p.s0_floor;
+      if (r.s > limit + 1e-12) {
+        const VRec sn = A[r.src];
+        const bool entered = r.lane != sn.lane;
+        const double floor_s = entered ? 0.0 : sn.s;
+        if (limit >= floor_s) {
+          r.v = py_max(0.0, py_min(r.v, r.v - (r.s - limit) / p.dt));
+          r.s = limit;
+        } else if (entered && !c.rs_reverted[j]) {
+          rev = j;
+          break;
+        } else if (prev >= 0 && C[prev].lane != A[C[prev].src].lane && !c.rs_reverted[prev]) {
+          rev = prev;
+          break;
+        } else {
+          r.v = 0.0;
+          r.s = floor_s;
+        }
+      }
+      prev = j;
+      prev_rear = r.s - p.L;
+    }
+    if (rev >= 0) {
+      reverts++;
+      VRec& r = C[rev];
+      const VRec sn = A[r.src];
+      const int32_t Lb = sn.lane;
+      const int32_t La = r.lane;
+      r.lane = sn.lane;  // _revert (world.py:501-507)
+      r.s = sn.s;
+      r.v = 0.0;
+      r.rp = sn.rp;
+      c.rs_reverted[rev] = 1;
+      c.rs_moved[nmoved++] = rev;
+      c.rs_movedin[Lb] = 1;
+      if (!c.rs_touched[Lb]) {
+        c.rs_touched[Lb] = 1;
+        c.rs_touched_list[nt++] = Lb;
+        if (Lb > reach && !c.rs_event[Lb]) {
+          // undo k_lanesort's tentative sweep: the reference sweeps Lb for
+          // the first time only now, with the reverted vehicle present
+          for (int32_t j = CS[Lb]; j < CS[Lb + 1]; j++) {
+            const VRec o = c.B[C[j].src];
+            C[j].s = o.s;
+            C[j].v = o.v;
+          }
+        }
+      }
+      if (!c.rs_inwork[La]) {
+        c.rs_inwork[La] = 1;
+        heap_push(heap, hn, La);
+      }
+      if (!c.rs_inwork[Lb]) {
+        c.rs_inwork[Lb] = 1;
+        heap_push(heap, hn, Lb);
+      }
+      if (reverts >= max_reverts) break;  // the reference's pass bound (world.py:518)
+    }
+  }
+  // clear scratch
+  for (int32_t q = 0; q < nt; q++) {
+    int32_t L = c.rs_touched_list[q];
+    c.rs_touched[L] = 0;
+    c.rs_event[L] = 0;
+    c.rs_movedin[L] = 0;
+    c.rs_inwork[L] = 0;
+  }
+  for (int32_t e = 0; e < ne; e++) {
+    c.rs_event[c.events[e]] = 0;
+    c.rs_inwork[c.events[e]] = 0;
+  }
+  for (int32_t q = 0; q < nmoved; q++) c.rs_reverted[c.rs_moved[q]] = 0;
+  dy->n_moved = nmoved;
+  dy->reverts_last = reverts;
+  // the resolve pass touched lanes out of order / moved vehicles
+  dy->need_regroup = 1;
+}
+
+// ------------------------------------------------------------------ signals + clock
+
+// Lane occupancy after the sweep (max-pressure input, world.py:634-637).
+__global__ void k_lane_counts(Ctx c) {
+  Dyn* dy = c.dyn;
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t n = dy->n_c;
+  for (int32_t i = gtid(); i < n; i += gstride()) atomicAdd(&c.lane_counts[C[i].lane], 1);
+}
+
+// world.py:619-647 (+ time/step increment, world.py:677-678).
+__global__ void k_signals(Ctx c) {
+  const Params& p = c.p;
+  for (int32_t j = gtid(); j < c.n_junc; j += gstride()) {
+    if (!c.junc_signal[j]) continue;
+    JuncState st = c.sig[j];
+    const int32_t b = c.junc_phase_off[j], np_ = c.junc_phase_off[j + 1] - b;
+    if (p.controller == 0) {
+      st.elapsed += p.dt;  // signals.advance_fixed (signals.py:37-43)
+      while (st.elapsed >= c.phase_dur[b + st.phase]) {
+        st.elapsed -= c.phase_dur[b + st.phase];
+        st.phase = (st.phase + 1) % np_;
+      }
+    } else {
+      st.elapsed += p.dt;
+      st.since += p.dt;
+      if (!(st.since < p.mp_interval || st.elapsed < p.mp_min_green)) {
+        int32_t best = 0;
+        long long best_p = 0;
+        bool have = false;
+        for (int32_t ph = 0; ph < np_; ph++) {  // signals.py:64-86
+          long long pr = 0;
+          for (int32_t q = c.jc_off[j]; q < c.jc_off[j + 1]; q++) {
+            int32_t cn = c.jc[q];
+            if ((c.green[cn] >> ph) & 1ULL) {
+              const LaneRec LR = c.lanes[cn];
+              pr += (long long)c.lane_counts[LR.pred1] - (long long)c.lane_counts[LR.succ1];
+            }
+          }
+          if (!have || pr > best_p) {
+            have = true;
+            best_p = pr;
+            best = ph;
+          }
+        }
+        if (best != st.phase) {
+          st.phase = best;
+          st.elapsed = 0.0;
+        }
+        st.since = 0.0;
+      }
+    }
+    c.sig[j] = st;
+  }
+}
+
+__global__ void k_clock(Ctx c) {
+  Dyn* dy = c.dyn;
+  dy->time += c.p.dt;
+  dy->step_no += 1;
+}
+
+// ------------------------------------------------------------------ injection (world.py:561-617)
+
+// Build the due list: retry (in due order) ++ pending with departure <= time.
+__global__ void k_inject_due(Ctx c) {
+  Dyn* dy = c.dyn;
+  __shared__ int32_t s_new;
+  const int32_t nr = dy->n_retry;
+  if (threadIdx.x == 0) {
+    const int32_t lo = dy->pend_ptr;
+    int32_t a = lo, b = c.n_trips;
+    const double t = dy->time;
+    while (a < b) {  // pending departures are non-decreasing
+      int32_t m = (a + b) >> 1;
+      if (c.pend_dep[m] <= t)
+        a = m + 1;
+      else
+        b = m;
+    }
+    s_new = a - lo;
+  }
+  __syncthreads();
+  const int32_t nn = s_new, lo = dy->pend_ptr;
+  for (int32_t k = threadIdx.x; k < nr; k += blockDim.x) c.due[k] = c.retry[k];
+  for (int32_t k = threadIdx.x; k < nn; k += blockDim.x) c.due[nr + k] = c.pend_vix[lo + k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dy->pend_ptr = lo + nn;
+    dy->n_due = nr + nn;
+    dy->n_retry = 0;
+  }
+}
+
+__global__ void k_inject_hist(Ctx c) {
+  Dyn* dy = c.dyn;
+  for (int32_t k = gtid(); k < dy->n_due; k += gstride()) atomicAdd(&c.inj_cnt[c.cold[c.due[k]].origin_lane], 1);
+}
+
+__global__ void k_inject_scatter(Ctx c) {
+  Dyn* dy = c.dyn;
+  for (int32_t k = gtid(); k < dy->n_due; k += gstride()) {
+    int32_t o = c.cold[c.due[k]].origin_lane;
+    int32_t pos = c.inj_start[o] + atomicAdd(&c.inj_cursor[o], 1);
+    c.due_grp[pos] = k;  // due position; sorted per lane below
+  }
+}
+
+// One thread per origin lane: candidates in due order, gap tests against the
+// lane's current occupants and the vehicles injected before them.
+__global__ void k_inject_lanes(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (dy->n_due == 0) return;
+  const Params& p = c.p;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const int32_t nmoved = dy->n_moved;
+  for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) {
+    const int32_t lo = c.inj_start[L], hi = c.inj_start[L + 1];
+    if (hi == lo) continue;
+    // insertion sort of due positions
+    for (int32_t a = lo + 1; a < hi; a++) {
+      int32_t x = c.due_grp[a], b = a - 1;
+      while (b >= lo && c.due_grp[b] > x) {
+        c.due_grp[b + 1] = c.due_grp[b];
+        b--;
+      }
+      c.due_grp[b + 1] = x;
+    }
+    const bool lane_open = c.lanes[L].open;
+    for (int32_t q = lo; q < hi; q++) {
+      const int32_t dpos = c.due_grp[q];
+      const int32_t vx = c.due[dpos];
+      const VCold cd = c.cold[vx];
+      uint8_t outc;
+      if (!c.routed[vx] && !lane_open) {
+        outc = OUT_RETRY;
+      } else if (!c.routed[vx] && cd.route_len <= 0) {
+        outc = OUT_DROP;
+        c.status[vx] = TSB_STATUS_DROPPED;
+        atomicAdd((unsigned long long*)&dy->dropped, 1ULL);
+      } else {
+        c.routed[vx] = 1;
+        const double o_s = cd.origin_s;
+        bool have_f = false, have_r = false;
+        double fs = 0.0, rs = 0.0;
+        auto consider = [&](double s) {
+          if (s >= o_s) {
+            if (!have_f || s < fs) {
+              fs = s;
+              have_f = true;
+            }
+          } else if (!have_r || s > rs) {
+            rs = s;
+            have_r = true;
+          }
+        };
+        for (int32_t j = CS[L]; j < CS[L + 1]; j++)
+          if (C[j].lane == L) consider(C[j].s);
+        for (int32_t q2 = 0; q2 < nmoved; q2++) {
+          const int32_t j = c.rs_moved[q2];
+          if (C[j].lane == L && (j < CS[L] || j >= CS[L + 1])) consider(C[j].s);
+        }
+        for (int32_t r = lo; r < q; r++)
+          if (c.outcome[c.due_grp[r]] == OUT_INJECT) consider(c.cold[c.due[c.due_grp[r]]].origin_s);
+        const double front_gap = have_f ? (fs - p.L) - o_s : CUDART_INF;
+        const double rear_gap = have_r ? (o_s - p.L) - rs : CUDART_INF;
+        if (front_gap < p.s0 + p.L || rear_gap < p.s0) {
+          outc = OUT_RETRY;
+        } else {
+          outc = OUT_INJECT;
+          int32_t k = atomicAdd(&dy->n_inj, 1);
+          VRec nr_{o_s, 0.0, vx, 0, L, -1};
+          C[dy->n_c + k] = nr_;
+          c.status[vx] = TSB_STATUS_DRIVING;
+        }
+      }
+      c.outcome[dpos] = outc;
+    }
+  }
+}
+
+__global__ void k_retry_flags(Ctx c) {
+  Dyn* dy = c.dyn;
+  for (int32_t k = gtid(); k < dy->n_due; k += gstride()) c.flag_in[k] = c.outcome[k] == OUT_RETRY ? 1 : 0;
+}
+
+__global__ void k_retry_compact(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t n = dy->n_due;
+  for (int32_t k = gtid(); k < n; k += gstride()) {
+    if (c.outcome[k] == OUT_RETRY) c.retry[c.flag_scan[k]] = c.due[k];
+    c.outcome[k] = OUT_NONE;
+  }
+}
+
+__global__ void k_inject_finish(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (dy->n_due > 0) dy->n_retry = c.flag_scan[dy->n_due];
+  dy->injected_now = dy->n_inj;
+  if (dy->n_inj > 0) dy->need_regroup = 1;
+}
+
+// ------------------------------------------------------------------ end of step
+
+// Choose the next snapshot: if nothing moved, C (already lane-sorted) is it.
+__global__ void k_commit_layout(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (!dy->need_regroup) {
+    dy->cur ^= 1;
+    dy->n_a = dy->n_c;
+  }
+}
+
+// Per road, over the new snapshot: sum v and count (world.py:649-657).
+// Warp per road, fixed-order tree reduction (deterministic).
+__global__ void k_speeds(Ctx c) {
+  Dyn* dy = c.dyn;
+  const VRec* A = c.lay[dy->cur];
+  const int32_t* S = c.start[dy->cur];
+  const int32_t wi = (int32_t)(dy->time / c.p.speed_window);
+  if (wi >= c.n_win) {
+    if (gtid() == 0) dy->overflow |= 2;
+    return;
+  }
+  const int lane_id = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int32_t r = gtid() >> 5; r < c.n_roads; r += warps) {
+    double sum = 0.0;
+    int32_t cnt = 0;
+    for (int32_t q = c.road_lane_off[r]; q < c.road_lane_off[r + 1]; q++) {
+      const int32_t L = c.road_lanes[q];
+      for (int32_t j = S[L] + lane_id; j < S[L + 1]; j += 32) {
+        sum += A[j].v;
+        cnt += 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane_id == 0 && cnt > 0) {
+      const size_t cell = (size_t)r * c.n_win + wi;
+      c.acc_sum[cell] += sum;
+      c.acc_cnt[cell] += cnt;
+    }
+  }
+}
+
+__global__ void k_end_step(Ctx c) {
+  Dyn* dy = c.dyn;
+  dy->finished_total += dy->finished_now;
+  dy->fin_log_n += dy->finished_now;
+}
+
+__global__ void k_begin_step(Ctx c) {
+  Dyn* dy = c.dyn;
+  dy->vehicle_updates += dy->n_a;
+  dy->finished_now = 0;
+  dy->n_events = 0;
+  dy->n_moved = 0;
+  dy->need_regroup = 0;
+  dy->n_inj = 0;
+  dy->n_hostq = 0;
+  dy->reverts_last = 0;
+  dy->n_due = 0;
+}
+
+// After the scans: vehicle totals from the last CSR entry.
+__global__ void k_set_nc(Ctx c) {
+  c.dyn->n_c = c.start[c.dyn->cur ^ 1][c.n_lanes];
+  if (c.dyn->n_hostq > 0 && !c.split) c.dyn->overflow |= 4;
+}
+__global__ void k_set_na(Ctx c, const int32_t* gate) {
+  if (gated_off(gate)) return;
+  c.dyn->n_a = c.start[c.dyn->cur][c.n_lanes];
+}
+
+// min_front_gap (world.py:694-704) over the snapshot layout.
+__global__ void k_min_gap(Ctx c, double* out) {
+  Dyn* dy = c.dyn;
+  const VRec* A = c.lay[dy->cur];
+  __shared__ double sm[32];
+  double best = CUDART_INF;
+  for (int32_t i = threadIdx.x; i + 1 < dy->n_a; i += blockDim.x)
+    if (A[i].lane == A[i + 1].lane) best = py_min(best, A[i].s - c.p.L - A[i + 1].s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++) best = fmin(best, sm[w]);
+    best = fmin(best, sm[0]);
+    *out = best;
+  }
+}
+
+}  // namespace tsb

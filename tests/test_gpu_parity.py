@@ -1,0 +1,78 @@
+"""GPU engine vs CPU oracle, step by step (bit-exact, correctly-rounded powers).
+
+The oracle (oracle/oracle.c) is pinned to the reference by test_oracle.py;
+here every step's full lane-sorted state (membership, order, road_pos, s, v),
+report counters, signal states, arrivals and statuses must be identical.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2405_12520_b200 import (EngineConfig, MAX_PRESSURE, Trip, generate_grid, make_corridor,
+                                   make_cross, make_ring, random_trips)
+from tests.parity import run_pair
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(*ws):
+    for w in ws:
+        w.close()
+
+
+def test_corridor_single_trip():
+    net = make_corridor()
+    o, d = net.roads["r0"][0], net.roads["r1"][0]
+    g, r, _ = run_pair(net, [Trip(0, o, 0.0, d, 5.0)], EngineConfig(), 0, 200)
+    assert len(g.finished) == 1
+    _close(g, r)
+
+
+def test_cross_signals_and_queues():
+    net = make_cross(arm=200.0, lane_count=2)
+    trips = random_trips(net, 120, seed=3, window=(0.0, 200.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 7, 400)
+    _close(g, r)
+
+
+def test_grid44_single_lane():
+    net = generate_grid(4, 4)
+    trips = random_trips(net, 1000, seed=42, window=(0.0, 3600.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 42, 600, every=5)
+    _close(g, r)
+
+
+def test_grid44_two_lanes_mobil():
+    net = generate_grid(4, 4, lanes_per_direction=2)
+    trips = random_trips(net, 2500, seed=42, window=(0.0, 700.0))
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 42, 1000, every=10)
+    _close(g, r)
+
+
+def test_jammed_grid_reverts():
+    net = generate_grid(4, 4)
+    trips = random_trips(net, 3000, seed=11, window=(0.0, 300.0))
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 11, 500, every=5)
+    _close(g, r)
+
+
+def test_max_pressure():
+    net = generate_grid(4, 4)
+    trips = random_trips(net, 400, seed=4, window=(0.0, 200.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(controller=MAX_PRESSURE), 4, 400, every=5)
+    _close(g, r)
+
+
+def test_ring_stop_and_go():
+    net = make_ring(100, radius=100 * 200.0 / (2 * np.pi))
+    import random
+    rng = random.Random(2024)
+    trips = []
+    roads = list(net.roads)
+    for k, rid in enumerate(roads):
+        lane = net.roads[rid][0]
+        dest = net.roads[roads[k - 1]][0]
+        for j in range(6):
+            trips.append(Trip(len(trips), lane, 22.0 * j + rng.uniform(0, 4), dest, 0.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 1, 300, every=3)
+    _close(g, r)
