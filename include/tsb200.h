@@ -101,6 +101,7 @@ typedef struct tsb_report {
   int64_t driving, waiting, finished, dropped, injected_now, finished_now;
   int64_t vehicle_updates; /* cumulative, world.py:663 */
   int64_t reverts_last;    /* collision-sweep reverts in the last step */
+  int64_t resolve_sequential; /* steps whose revert chains needed the sequential replay */
 } tsb_report;
 
 typedef struct tsb_engine tsb_engine;
@@ -165,6 +166,9 @@ int tsb_profile_steps(tsb_engine* e, int32_t n_steps, int32_t cap, double* kerne
 const char* tsb_kernel_name(int32_t k);
 /* Device time (ms) of n graph-replayed steps bracketed by CUDA events. */
 int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms);
+/* Test knobs: bit 0 forces the sequential revert-chain resolver, bit 1 the
+ * full (non-incremental) regroup.  Results must not change. */
+int tsb_set_debug(tsb_engine* e, int32_t flags);
 /* Kernel launches issued per step (for the bench's gpu_launches claim). */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);
 

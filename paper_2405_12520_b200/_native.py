@@ -43,6 +43,7 @@ SIGNATURES = {
     "tsb_kernel_name": (C.c_char_p, [_i32]),
     "tsb_time_steps": (_i32, [_vp, _i32, C.POINTER(_f64)]),
     "tsb_launches_per_step": (_i32, [_vp, C.POINTER(_i32)]),
+    "tsb_set_debug": (_i32, [_vp, _i32]),
 }
 
 _lib = None

@@ -58,7 +58,8 @@ class TsbParams(C.Structure):
 class TsbReport(C.Structure):
     _fields_ = [("time", C.c_double), ("step_no", C.c_int64)] + [
         (k, C.c_int64) for k in ("driving", "waiting", "finished", "dropped", "injected_now",
-                                 "finished_now", "vehicle_updates", "reverts_last")]
+                                 "finished_now", "vehicle_updates", "reverts_last",
+                                 "resolve_sequential")]
 
 
 _CT = {np.float64: C.c_double, np.int8: C.c_int8, np.uint8: C.c_uint8,

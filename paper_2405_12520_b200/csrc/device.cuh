@@ -84,6 +84,10 @@ struct Dyn {
   int32_t n_events;     // lanes whose tentative sweep hit a revert
   int32_t n_moved;      // vehicles moved by resolve (reverted into another lane)
   int32_t need_regroup; // membership or order changed after the sweep
+  int32_t complex;      // some revert event is not simple: sequential resolve
+  int32_t n_dirty;      // lanes rebuilt by the incremental regroup
+  int32_t full_regroup; // too many dirty lanes: full regroup instead
+  int64_t resolve_sequential;  // steps that needed the sequential resolver
   int32_t pend_ptr;
   int32_t n_retry;
   int32_t n_due;
@@ -108,6 +112,7 @@ struct Ctx {
   Params p;
   int32_t n_lanes, n_roads, n_junc, n_trips;
   int32_t split;  // 1 when lane closures exist: host continuation of reroutes
+  int32_t debug;  // test knobs: 1 = always sequential resolve, 2 = always full regroup
   const LaneRec* lanes;
   const int32_t* succ;
   const int32_t* succ_dst_road;
@@ -137,6 +142,14 @@ struct Ctx {
   int32_t scan_tiles_cap;
   int32_t* stage;  // scan staging (n_lanes + 1)
   int32_t* events;
+  int32_t* ev_x;     // per event: C index of the reverted vehicle
+  int32_t* ev_lb;    // per event: its snapshot lane (revert target)
+  int32_t* tcount;   // per lane: events targeting it
+  int32_t* dirty_flag;
+  int32_t* dirty_list;
+  int32_t* patch_lanes;
+  int32_t* patch_count;
+  int32_t* patch_prefix;
   // resolve scratch
   int32_t* rs_heap;
   uint8_t* rs_inwork;

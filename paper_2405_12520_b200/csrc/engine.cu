@@ -174,6 +174,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_MISC, k_set_nc, 1, 1, c);
   LAUNCH(KC_SCATTER, k_scatter, vgrid, VB, c, SEL_B, &dy->n_a, nullptr, SEL_C, nullptr);
   LAUNCH(KC_LANESORT_SWEEP, k_lanesort<true>, wgrid, VB, c, SEL_C, nullptr);
+  LAUNCH(KC_RESOLVE, k_resolve_find, 148, 256, c);
+  LAUNCH(KC_RESOLVE, k_resolve_check, 296, 128, c);
+  LAUNCH(KC_RESOLVE, k_resolve_apply, 296, 128, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
   if (c.p.controller == 1) {
     cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->stream);
@@ -193,14 +196,20 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   scan(e, L, KC_INJECT, c.flag_in, c.flag_scan, SEL_NONE, &dy->n_due, 0, e->n_trips, &dy->n_due);
   LAUNCH(KC_INJECT, k_retry_compact, vgrid, VB, c);
   LAUNCH(KC_INJECT, k_inject_finish, 1, 1, c);
-  // next snapshot: full regroup only if membership / order changed
+  // next snapshot: nothing if no lane changed membership/order; else rebuild
+  // only the dirty lanes and shift the rest; full regroup if too many changed
+  LAUNCH(KC_REGROUP, k_patch_prepare, 1, 1024, c);
+  LAUNCH(KC_REGROUP, k_patch_starts, tgrid, VB, c);
+  LAUNCH(KC_REGROUP, k_patch_copy, vgrid, VB, c);
+  LAUNCH(KC_REGROUP, k_patch_dirty, 64, VB, c);
   cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->stream);
   cudaMemsetAsync(c.cursor, 0, sizeof(int32_t) * NL, e->stream);
-  LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->need_regroup);
-  scan(e, L, KC_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->need_regroup);
-  LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->need_regroup);
-  LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->need_regroup);
-  LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->need_regroup);
+  LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->full_regroup);
+  scan(e, L, KC_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->full_regroup);
+  LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
+  LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
+  LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
+  LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
   LAUNCH(KC_MISC, k_commit_layout, 1, 1, c);
   LAUNCH(KC_SPEEDS, k_speeds, rgrid, VB, c);
   LAUNCH(KC_MISC, k_end_step, 1, 1, c);
@@ -622,6 +631,14 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.scan_tiles, 1));
   RC(dalloc(E, &c.stage, (size_t)NL + 1));
   RC(dalloc(E, &c.events, NL));
+  RC(dalloc(E, &c.ev_x, NL));
+  RC(dalloc(E, &c.ev_lb, NL));
+  RC(dalloc(E, &c.tcount, NL));
+  RC(dalloc(E, &c.dirty_flag, NL));
+  RC(dalloc(E, &c.dirty_list, NL));
+  RC(dalloc(E, &c.patch_lanes, 4096));
+  RC(dalloc(E, &c.patch_count, 4096));
+  RC(dalloc(E, &c.patch_prefix, 4097));
   RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)N + 16));
   RC(dalloc(E, &c.rs_inwork, NL));
   RC(dalloc(E, &c.rs_touched, NL));
@@ -694,6 +711,7 @@ static void fill_report(const tsb_engine* e, tsb_report* r) {
   r->finished_now = d.finished_now;
   r->vehicle_updates = d.vehicle_updates;
   r->reverts_last = d.reverts_last;
+  r->resolve_sequential = d.resolve_sequential;
 }
 
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last) {
@@ -913,6 +931,12 @@ int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   RC(sync_dyn(e));
+  return TSB_OK;
+}
+
+int tsb_set_debug(tsb_engine* e, int32_t flags) {
+  e->c.debug = flags;
+  e->graph_dirty = true;
   return TSB_OK;
 }
 

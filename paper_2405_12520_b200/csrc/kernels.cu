@@ -51,6 +51,16 @@ __device__ __forceinline__ int32_t* start_buf(const Ctx& c, int sel) {
 }
 __device__ __forceinline__ bool gated_off(const int32_t* gate) { return gate && *gate == 0; }
 
+// A lane whose membership or order changed after the sweep; the next
+// snapshot rebuilds only these lanes (k_patch_*), unless too many changed.
+__device__ __forceinline__ void mark_dirty(const Ctx& c, int32_t L) {
+  if (atomicExch(&c.dirty_flag[L], 1) == 0) {
+    int32_t k = atomicAdd(&c.dyn->n_dirty, 1);
+    c.dirty_list[k] = L;
+  }
+  c.dyn->need_regroup = 1;
+}
+
 // ------------------------------------------------------------------ network helpers
 
 // _conn_from[(lane, road)] (world.py:155-166): smallest successor connector
@@ -593,10 +603,246 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
         // a hold can break the (s desc) order; the next snapshot must be re-sorted
         for (int32_t q = (first > 0 ? first - 1 : 0); q + 1 < n; q++)
           if (!ahead_of(C[lo + q].s, C[lo + q].vix, C[lo + q + 1].s, C[lo + q + 1].vix)) {
-            dy->need_regroup = 1;
+            mark_dirty(c, L);
             break;
           }
       }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ resolve fast path
+//
+// When every revert event is "simple" -- its lane La and target lane Lb are
+// touched by no other event, Lb is not itself an event lane, and neither the
+// re-sweep of La (without the reverted vehicle) nor the sweep of Lb (with it)
+// reverts again -- the reference's restart order reduces to independent
+// per-event work: events are processed in increasing lane order, so the
+// reach when event La reverts is exactly La, and Lb is restored to its
+// post-delta state iff Lb > La.  R1 finds each event's reverted vehicle,
+// R2 checks simplicity (any failure sets dyn->complex and the sequential
+// k_resolve replays everything from the untouched state), R3 applies.
+
+struct SwM {
+  double s, v, snap_s;
+  int32_t j;        // index in C
+  int32_t vix;
+  uint8_t entered;  // lane != snapshot lane
+  uint8_t reverted;
+  uint8_t pad[2];
+};
+static constexpr int SW_CAP = 96;  // members per lane handled by the fast path
+
+// The reference's lane sweep (world.py:527-555) over m[0..n) sorted front
+// first; applies clamps/holds in place and returns the member to revert, or -1.
+__device__ int sweep_members(SwM* m, int n, const Params& p) {
+  int prev = -1;
+  double prev_rear = CUDART_INF;
+  for (int a = 0; a < n; a++) {
+    const double limit = prev_rear - p.s0_floor;
+    if (m[a].s > limit + 1e-12) {
+      const double floor_s = m[a].entered ? 0.0 : m[a].snap_s;
+      if (limit >= floor_s) {
+        m[a].v = py_max(0.0, py_min(m[a].v, m[a].v - (m[a].s - limit) / p.dt));
+        m[a].s = limit;
+      } else if (m[a].entered && !m[a].reverted) {
+        return a;
+      } else if (prev >= 0 && m[prev].entered && !m[prev].reverted) {
+        return prev;
+      } else {
+        m[a].v = 0.0;
+        m[a].s = floor_s;
+      }
+    }
+    prev = a;
+    prev_rear = m[a].s - p.L;
+  }
+  return -1;
+}
+
+// Load lane L's segment of C (entries still on L) into m; values from C or,
+// if `original`, from the post-delta B.  Returns count or -1 if over SW_CAP.
+__device__ int load_lane(const Ctx& c, const VRec* C, const int32_t* CS, const VRec* A, int32_t L, bool original,
+                         SwM* m) {
+  const int lane_id = threadIdx.x & 31;
+  const int32_t lo = CS[L], hi = CS[L + 1];
+  if (hi - lo > SW_CAP) return -1;
+  for (int32_t j = lo + lane_id; j < hi; j += 32) {
+    VRec r = C[j];
+    const VRec sn = A[r.src];
+    SwM x;
+    if (original) {
+      const VRec o = c.B[r.src];
+      x.s = o.s;
+      x.v = o.v;
+    } else {
+      x.s = r.s;
+      x.v = r.v;
+    }
+    x.snap_s = sn.s;
+    x.j = j;
+    x.vix = r.vix;
+    x.entered = r.lane != sn.lane;
+    x.reverted = 0;
+    m[j - lo] = x;
+  }
+  __syncwarp();
+  return hi - lo;
+}
+
+// Sort m[0..n) by (s desc, vix asc) with a warp rank sort through `tmp`.
+__device__ void sort_members(SwM* m, SwM* tmp, int n) {
+  const int lane_id = threadIdx.x & 31;
+  for (int a = lane_id; a < n; a += 32) tmp[a] = m[a];
+  __syncwarp();
+  for (int a = lane_id; a < n; a += 32) {
+    int rank = 0;
+    for (int b = 0; b < n; b++) rank += ahead_of(tmp[b].s, tmp[b].vix, tmp[a].s, tmp[a].vix) ? 1 : 0;
+    m[rank] = tmp[a];
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_resolve_find(Ctx c) {
+  __shared__ SwM sm[8][SW_CAP];
+  Dyn* dy = c.dyn;
+  const int ne = dy->n_events;
+  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
+    const int32_t La = c.events[e];
+    int n = load_lane(c, C, CS, A, La, false, sm[w]);
+    int32_t jx = -1, lb = -1;
+    if (n > 0 && lane_id == 0) {
+      int x = sweep_members(sm[w], n, c.p);
+      if (x >= 0) {
+        jx = sm[w][x].j;
+        lb = A[C[jx].src].lane;
+      }
+    }
+    if (lane_id == 0) {
+      c.ev_x[e] = jx;
+      c.ev_lb[e] = lb;
+      c.rs_event[La] = 1;
+      if (lb >= 0)
+        atomicAdd(&c.tcount[lb], 1);
+      if (lb < 0 || (c.debug & 1)) dy->complex = 1;  // oversized lane / forced: sequential path
+    }
+    __syncwarp();
+  }
+}
+
+// Simulates (apply=false) or applies (apply=true) one simple event.
+__device__ bool simple_event(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, int e, SwM* m, SwM* tmp,
+                             bool apply) {
+  const int lane_id = threadIdx.x & 31;
+  Dyn* dy = c.dyn;
+  const int32_t La = c.events[e], jx = c.ev_x[e], Lb = c.ev_lb[e];
+  // La: sweep to the revert, drop the reverted vehicle, re-sweep from the front
+  int n = load_lane(c, C, CS, A, La, false, m);
+  int ok = 1;
+  if (lane_id == 0) {
+    int x = sweep_members(m, n, c.p);
+    if (x < 0 || m[x].j != jx) ok = 0;
+    if (ok) {
+      for (int a = x; a + 1 < n; a++) m[a] = m[a + 1];
+      n -= 1;
+      if (sweep_members(m, n, c.p) >= 0) ok = 0;
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  n = __shfl_sync(0xffffffffu, n, 0);
+  if (!ok) return false;
+  if (apply) {
+    for (int a = lane_id; a < n; a += 32) {
+      C[m[a].j].s = m[a].s;
+      C[m[a].j].v = m[a].v;
+    }
+  }
+  __syncwarp();
+  // Lb: its state when the reference sweeps it next, plus the reverted vehicle
+  int nb = load_lane(c, C, CS, A, Lb, Lb > La, m);
+  if (nb < 0 || nb + 1 > SW_CAP) return false;
+  const VRec rx = C[jx];
+  const VRec sx = A[rx.src];
+  if (lane_id == 0) {
+    SwM x;
+    x.s = sx.s;
+    x.v = 0.0;
+    x.snap_s = sx.s;
+    x.j = jx;
+    x.vix = rx.vix;
+    x.entered = 0;
+    x.reverted = 1;
+    m[nb] = x;
+  }
+  __syncwarp();
+  nb += 1;
+  sort_members(m, tmp, nb);
+  if (lane_id == 0) ok = sweep_members(m, nb, c.p) < 0;
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (!ok) return false;
+  if (apply) {
+    for (int a = lane_id; a < nb; a += 32) {
+      const int32_t j = m[a].j;
+      C[j].s = m[a].s;
+      C[j].v = m[a].v;
+    }
+    __syncwarp();
+    if (lane_id == 0) {
+      C[jx].lane = Lb;  // _revert (world.py:501-507); s, v set by the sweep above
+      C[jx].rp = sx.rp;
+      const int32_t q = atomicAdd(&dy->n_moved, 1);
+      c.rs_moved[q] = jx;
+      c.rs_movedin[Lb] = 1;
+      atomicAdd((unsigned long long*)&dy->reverts_last, 1ULL);
+      mark_dirty(c, La);
+      mark_dirty(c, Lb);
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(128) k_resolve_check(Ctx c) {
+  __shared__ SwM sm[4][SW_CAP];
+  __shared__ SwM tm[4][SW_CAP];
+  Dyn* dy = c.dyn;
+  const int ne = dy->n_events;
+  if (ne == 0 || dy->complex) return;
+  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
+    const int32_t La = c.events[e], Lb = c.ev_lb[e];
+    bool ok = !c.rs_event[Lb] && c.tcount[Lb] == 1 && c.tcount[La] == 0;
+    if (ok) ok = simple_event(c, C, CS, A, e, sm[w], tm[w], false);
+    if (!ok && lane_id == 0) dy->complex = 1;
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(128) k_resolve_apply(Ctx c) {
+  __shared__ SwM sm[4][SW_CAP];
+  __shared__ SwM tm[4][SW_CAP];
+  Dyn* dy = c.dyn;
+  const int ne = dy->n_events;
+  if (ne == 0) return;
+  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  const bool cx = dy->complex;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
+    if (lane_id == 0) {
+      if (c.ev_lb[e] >= 0) c.tcount[c.ev_lb[e]] = 0;
+    }
+    if (!cx) {
+      simple_event(c, C, CS, A, e, sm[w], tm[w], true);
+      if (lane_id == 0) c.rs_event[c.events[e]] = 0;
     }
     __syncwarp();
   }
@@ -644,7 +890,9 @@ __device__ int32_t heap_pop(int32_t* h, int32_t& n) {
 __global__ void k_resolve(Ctx c) {
   Dyn* dy = c.dyn;
   const int32_t ne = dy->n_events;
-  if (ne == 0 || threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (ne == 0 || !dy->complex || threadIdx.x != 0 || blockIdx.x != 0) return;
+  dy->n_moved = 0;
+  dy->reverts_last = 0;
   const Params& p = c.p;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
@@ -754,7 +1002,8 @@ __global__ void k_resolve(Ctx c) {
       if (reverts >= max_reverts) break;  // the reference's pass bound (world.py:518)
     }
   }
-  // clear scratch
+  // clear scratch; every touched lane is rebuilt in the next snapshot
+  for (int32_t q = 0; q < nt; q++) mark_dirty(c, c.rs_touched_list[q]);
   for (int32_t q = 0; q < nt; q++) {
     int32_t L = c.rs_touched_list[q];
     c.rs_touched[L] = 0;
@@ -769,8 +1018,7 @@ __global__ void k_resolve(Ctx c) {
   for (int32_t q = 0; q < nmoved; q++) c.rs_reverted[c.rs_moved[q]] = 0;
   dy->n_moved = nmoved;
   dy->reverts_last = reverts;
-  // the resolve pass touched lanes out of order / moved vehicles
-  dy->need_regroup = 1;
+  dy->resolve_sequential += 1;
 }
 
 // ------------------------------------------------------------------ signals + clock
@@ -948,6 +1196,7 @@ __global__ void k_inject_lanes(Ctx c) {
           VRec nr_{o_s, 0.0, vx, 0, L, -1};
           C[dy->n_c + k] = nr_;
           c.status[vx] = TSB_STATUS_DRIVING;
+          mark_dirty(c, L);
         }
       }
       c.outcome[dpos] = outc;
@@ -973,7 +1222,160 @@ __global__ void k_inject_finish(Ctx c) {
   Dyn* dy = c.dyn;
   if (dy->n_due > 0) dy->n_retry = c.flag_scan[dy->n_due];
   dy->injected_now = dy->n_inj;
-  if (dy->n_inj > 0) dy->need_regroup = 1;
+}
+
+// ------------------------------------------------------------------ incremental regroup
+
+static constexpr int PATCH_MAX = 4096;  // dirty lanes handled by the patch path
+
+// Members of dirty lane L in the post-sweep layout C: segment entries still on
+// L, vehicles reverted into L, vehicles injected into L (C tail).
+template <class F>
+__device__ void for_members(const Ctx& c, const VRec* C, const int32_t* CS, int32_t L, F f) {
+  const Dyn* dy = c.dyn;
+  const int lane_id = threadIdx.x & 31;
+  for (int32_t j = CS[L] + lane_id; j < CS[L + 1]; j += 32)
+    if (C[j].lane == L) f(j);
+  for (int32_t q = lane_id; q < dy->n_moved; q += 32) {
+    const int32_t j = c.rs_moved[q];
+    if (C[j].lane == L && (j < CS[L] || j >= CS[L + 1])) f(j);
+  }
+  for (int32_t j = dy->n_c + lane_id; j < dy->n_c + dy->n_inj; j += 32)
+    if (C[j].lane == L) f(j);
+}
+
+// One block: decide patch vs full regroup; sort dirty lanes; new counts and
+// the prefix of count deltas in lane order.
+__global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int nd = dy->n_dirty;
+  if (!dy->need_regroup) return;
+  if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
+    if (threadIdx.x == 0) dy->full_regroup = 1;
+    return;
+  }
+  __shared__ int32_t sl[PATCH_MAX];
+  __shared__ int32_t sd[PATCH_MAX];
+  __shared__ int32_t warp_sum[32];
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) sl[i] = c.dirty_list[i];
+  __syncthreads();
+  // rank sort of the (distinct) dirty lane ids
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    const int32_t x = sl[i];
+    int r = 0;
+    for (int q = 0; q < nd; q++) r += sl[q] < x ? 1 : 0;
+    c.patch_lanes[r] = x;
+  }
+  __syncthreads();
+  // new member count of each dirty lane (warp per lane)
+  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  for (int i = w; i < nd; i += blockDim.x >> 5) {
+    const int32_t L = c.patch_lanes[i];
+    int cnt = 0;
+    for_members(c, C, CS, L, [&](int32_t) { cnt++; });
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane_id == 0) {
+      c.patch_count[i] = cnt;
+      sd[i] = cnt - (CS[L + 1] - CS[L]);
+    }
+  }
+  __syncthreads();
+  // exclusive prefix of deltas (serial per chunk is fine: nd <= 4096)
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int i = 0; i < nd; i++) {
+      c.patch_prefix[i] = run;
+      run += sd[i];
+    }
+    c.patch_prefix[nd] = run;
+  }
+  (void)warp_sum;
+}
+
+__device__ __forceinline__ int32_t dirty_below(const int32_t* lanes, int nd, int32_t L) {
+  int a = 0, b = nd;
+  while (a < b) {
+    int m = (a + b) >> 1;
+    if (lanes[m] < L)
+      a = m + 1;
+    else
+      b = m;
+  }
+  return a;
+}
+
+// new_start[L] = C_start[L] + (sum of count deltas of dirty lanes < L)
+__global__ void k_patch_starts(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (!dy->need_regroup || dy->full_regroup) return;
+  const int nd = dy->n_dirty;
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  int32_t* AS = c.start[dy->cur];
+  for (int32_t L = gtid(); L <= c.n_lanes; L += gstride()) {
+    const int k = dirty_below(c.patch_lanes, nd, L);
+    AS[L] = CS[L] + c.patch_prefix[k];
+  }
+}
+
+// Clean lanes keep their sorted segments, shifted.
+__global__ void k_patch_copy(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (!dy->need_regroup || dy->full_regroup) return;
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  VRec* A = c.lay[dy->cur];
+  const int32_t* AS = c.start[dy->cur];
+  const int32_t n = dy->n_c;
+  for (int32_t j = gtid(); j < n; j += gstride()) {
+    const VRec r = C[j];
+    if (c.dirty_flag[r.lane]) continue;
+    A[AS[r.lane] + (j - CS[r.lane])] = r;
+  }
+}
+
+// Dirty lanes: gather members, sort (s desc, id asc), write.  Warp per lane.
+__global__ void k_patch_dirty(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (!dy->need_regroup || dy->full_regroup) return;
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  VRec* A = c.lay[dy->cur];
+  const int32_t* AS = c.start[dy->cur];
+  const int nd = dy->n_dirty;
+  const int lane_id = threadIdx.x & 31;
+  for (int i = gtid() >> 5; i < nd; i += gstride() >> 5) {
+    const int32_t L = c.patch_lanes[i];
+    const int32_t base = AS[L];
+    const int32_t n = c.patch_count[i];
+    // pass 1: collect member indices into the destination range's vix slots
+    // (rank computed against all members; members are few)
+    int pos = 0;
+    for_members(c, C, CS, L, [&](int32_t j) {
+      const VRec r = C[j];
+      int rank = 0;
+      // count members ahead of r
+      for (int32_t q = CS[L]; q < CS[L + 1]; q++)
+        if (C[q].lane == L && ahead_of(C[q].s, C[q].vix, r.s, r.vix)) rank++;
+      for (int32_t q = 0; q < dy->n_moved; q++) {
+        const int32_t jj = c.rs_moved[q];
+        if (C[jj].lane == L && (jj < CS[L] || jj >= CS[L + 1]) && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix)) rank++;
+      }
+      for (int32_t jj = dy->n_c; jj < dy->n_c + dy->n_inj; jj++)
+        if (C[jj].lane == L && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix)) rank++;
+      if (rank < n) A[base + rank] = r;
+      pos++;
+    });
+    (void)pos;
+  }
+}
+
+__global__ void k_patch_finish(Ctx c) {
+  Dyn* dy = c.dyn;
+  if (dy->need_regroup && !dy->full_regroup) dy->n_a = dy->n_c + dy->n_inj;
+  // clear dirty flags for the next step
+  for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) c.dirty_flag[c.dirty_list[i]] = 0;
 }
 
 // ------------------------------------------------------------------ end of step
@@ -1034,6 +1436,9 @@ __global__ void k_begin_step(Ctx c) {
   dy->vehicle_updates += dy->n_a;
   dy->finished_now = 0;
   dy->n_events = 0;
+  dy->complex = 0;
+  dy->n_dirty = 0;
+  dy->full_regroup = 0;
   dy->n_moved = 0;
   dy->need_regroup = 0;
   dy->n_inj = 0;

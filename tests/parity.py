@@ -33,8 +33,11 @@ def compare_reports(gpu: World, ref: OracleWorld, step: int):
         assert getattr(g, k) == getattr(r, k), f"step {step}: report.{k} {getattr(g, k)} vs {getattr(r, k)}"
 
 
-def run_pair(net, trips, config, seed, steps, exact=True, every=1, check_signals=True):
+def run_pair(net, trips, config, seed, steps, exact=True, every=1, check_signals=True, debug=0):
     gpu = World(net, trips, config, seed=seed)
+    if debug:
+        from paper_2405_12520_b200 import _native
+        _native.check(_native.lib().tsb_set_debug(gpu._h, debug))
     ref = OracleWorld(net, trips, config, seed=seed, pow_mode=0 if exact else 1)
     reverts = 0
     try:

@@ -76,3 +76,24 @@ def test_ring_stop_and_go():
             trips.append(Trip(len(trips), lane, 22.0 * j + rng.uniform(0, 4), dest, 0.0))
     g, r, _ = run_pair(net, trips, EngineConfig(), 1, 300, every=3)
     _close(g, r)
+
+
+@pytest.mark.parametrize("debug", [0, 1, 2, 3])
+def test_dense_short_blocks_revert_chains(debug):
+    """Up to 35 reverts per step: parallel fast path, forced sequential
+    replay (bit 0) and forced full regroup (bit 1) must all match the oracle."""
+    net = generate_grid(6, 6, block_length=60.0)
+    trips = random_trips(net, 6000, seed=5, window=(0.0, 200.0))
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 5, 400, every=2, debug=debug)
+    assert reverts > 200
+    print("reverts", reverts, "sequential-resolve steps", g._report.resolve_sequential)
+    _close(g, r)
+
+
+def test_dense_two_lane_reverts():
+    net = generate_grid(5, 5, block_length=80.0, lanes_per_direction=2)
+    trips = random_trips(net, 6000, seed=5, window=(0.0, 300.0))
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 5, 400, every=2)
+    assert reverts > 50
+    print("reverts", reverts, "sequential-resolve steps", g._report.resolve_sequential)
+    _close(g, r)
