@@ -237,6 +237,8 @@ def main():
         if nk < 0:
             _native.check(nk)
     clocks = clk.summary()
+    r_end = world._report
+    _native.check(L.tsb_report_get(world._h, C.byref(r_end)))
     launches = C.c_int32()
     _native.check(L.tsb_launches_per_step(world._h, C.byref(launches)))
 
@@ -273,7 +275,9 @@ def main():
                    "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single",
                    "l2": "no flush: per-step working set (4 x 32 MB vehicle layouts + route gathers + "
                          "15 MB lane table) exceeds the 126 MB L2",
-                   "timing": "CUDA events on the engine stream around K graph replays"},
+                   "timing": "CUDA events on the engine stream around K graph replays",
+                   "reverts_per_step": r_end.reverts_total / max(1, r_end.step_no),
+                   "sequential_resolve_steps": r_end.resolve_sequential, "steps_total": r_end.step_no},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": C.sizeof(r),
                 "how": "World.step() loop (reference API), wall clock; each step syncs and copies its "

@@ -102,6 +102,7 @@ typedef struct tsb_report {
   int64_t vehicle_updates; /* cumulative, world.py:663 */
   int64_t reverts_last;    /* collision-sweep reverts in the last step */
   int64_t resolve_sequential; /* steps whose revert chains needed the sequential replay */
+  int64_t reverts_total;      /* collision-sweep reverts, cumulative */
 } tsb_report;
 
 typedef struct tsb_engine tsb_engine;

@@ -109,7 +109,7 @@ struct orc {
   ivec fin_vix;
   double* fin_t;
   int64_t fin_cap;
-  int64_t dropped, vehicle_updates, step_no, injected_now, finished_now, reverts_last;
+  int64_t dropped, vehicle_updates, step_no, injected_now, finished_now, reverts_last, reverts_total;
   double time;
   /* speed accumulators [road][window] */
   int32_t nwin;
@@ -772,7 +772,10 @@ static void collision_sweep(orc* o) {
       }
       i = j;
     }
-    if (dirty) o->reverts_last++;
+    if (dirty) {
+      o->reverts_last++;
+      o->reverts_total++;
+    }
     if (!dirty) break;
   }
   free(grp);
@@ -1073,6 +1076,7 @@ static void fill_report(const orc* o, tsb_report* r) {
   r->finished_now = o->finished_now;
   r->vehicle_updates = o->vehicle_updates;
   r->reverts_last = o->reverts_last;
+  r->reverts_total = o->reverts_total;
 }
 
 int orc_step(orc* o, int32_t n, tsb_report* last) {

@@ -59,7 +59,7 @@ class TsbReport(C.Structure):
     _fields_ = [("time", C.c_double), ("step_no", C.c_int64)] + [
         (k, C.c_int64) for k in ("driving", "waiting", "finished", "dropped", "injected_now",
                                  "finished_now", "vehicle_updates", "reverts_last",
-                                 "resolve_sequential")]
+                                 "resolve_sequential", "reverts_total")]
 
 
 _CT = {np.float64: C.c_double, np.int8: C.c_int8, np.uint8: C.c_uint8,

@@ -17,16 +17,29 @@ namespace tsb {
 // One driving vehicle in a lane-sorted layout (32 B, two 16 B vectors).
 // `lane` is explicit (the CSR position implies it, but the update kernel
 // needs it without a search); `src` is the index of the vehicle in the
-// step's snapshot layout A, which carries the snapshot lane/s/rp needed by
+// step's snapshot layout A, which carries the snapshot lane/s/rptr needed by
 // the collision sweep and by reverts (world.py:501-507).
+// `rptr` replaces the reference's road_pos: it is the absolute index in the
+// route pool of roads_seq[road_pos].  Every route in the pool is followed by
+// a -1 sentinel, so "on the final road" (world.py:276, 455) is
+// routes[rptr + 1] < 0 and the update never gathers per-vehicle route
+// metadata; road_pos = rptr - route_off[vix] is recovered on the host.
 struct __align__(16) VRec {
   double s;
   double v;
   int32_t vix;
-  int32_t rp;
+  int32_t rptr;
   int32_t lane;
   int32_t src;
 };
+
+// Per-lane flag byte (lflag[]), read by the update instead of chains of
+// LaneRec / signal-state gathers.  Bit 0 (OPEN) is the lane's own
+// restriction (host-maintained); for connectors, bit 1 (SUCC_OPEN) is the
+// restriction of its successor road lane and bits 2-3 its signal aspect
+// (world.py:247-254, signals.py:46-61), refreshed by k_signals each step and
+// by k_lane_flags after a control change.
+enum : uint8_t { LF_OPEN = 1, LF_SUCC_OPEN = 2, LF_ASPECT_SHIFT = 2 };
 
 // Static per-lane record (48 B) gathered by the update kernel.
 struct __align__(16) LaneRec {
@@ -94,6 +107,9 @@ struct Dyn {
   int32_t n_hostq;      // vehicles needing a host reroute (closures only)
   int32_t overflow;     // sticky error flag
   int64_t fin_log_n;
+  int64_t reverts_total;
+  int32_t n_cl;    // lanes in the revert closure (cleared at the next step)
+  int32_t n_comp;  // closure components replayed in parallel
 };
 
 struct Params {
@@ -126,6 +142,9 @@ struct Ctx {
   const int32_t* jc;
   JuncState* sig;
   const VCold* cold;
+  const uint64_t* keys;  // RNG key per vix (id & (2^64-1)); unused when ids_dense
+  int32_t ids_dense;     // 1 when id == vix for every trip: key = vix
+  uint8_t* lflag;
   const int32_t* routes;
   uint8_t* status;
   uint8_t* routed;
@@ -142,9 +161,15 @@ struct Ctx {
   int32_t scan_tiles_cap;
   int32_t* stage;  // scan staging (n_lanes + 1)
   int32_t* events;
-  int32_t* ev_x;     // per event: C index of the reverted vehicle
-  int32_t* ev_lb;    // per event: its snapshot lane (revert target)
-  int32_t* tcount;   // per lane: events targeting it
+  // revert closure / components (k_resolve_closure)
+  int32_t* cl_idx;    // per lane: 1 + index in the closure, 0 = outside
+  int32_t* cl_lanes;  // closure lanes of the current step
+  int32_t* comp_id;
+  int32_t* comp_off;
+  int32_t* comp_size;
+  int32_t* comp_edges;
+  int32_t* comp_fill;
+  int32_t* comp_ev;
   int32_t* dirty_flag;
   int32_t* dirty_list;
   int32_t* patch_lanes;
@@ -218,20 +243,46 @@ __device__ __forceinline__ double pow_int_cr(double x, int n) {
   return rh + rl;
 }
 
-// idm.py:17-31.  (s*/gap)**2 is the correctly rounded square, i.e. q*q.
-__device__ __forceinline__ double idm_accel(const Params& p, double v, double dv, double gap, double v_cap) {
-  double v0_eff = py_min(p.v0, v_cap);
-  double x = v / v0_eff;
-  double fr = p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
-  double inter;
-  if (isinf(gap)) {
-    inter = 0.0;
-  } else {
-    double s_star = p.s0 + py_max(0.0, v * p.T + v * dv / p.sqrt_ab2);
-    double q = s_star / gap;
-    inter = q * q;
-  }
+// x / y for y > 0 (finite, nonzero).  IEEE gives x exactly (signed zero
+// kept) when x == 0.  A zero numerator sends the inline division to its
+// out-of-line slow path (stopped vehicles, v == 0, are the common case in
+// queues: that call dominated the update kernel, profiles/r1a_*), and a
+// plain `x == 0 ? x : x / y` does not help because the compiler speculates
+// the division.  Dividing an opaque copy of (z ? 1.0 : x) -- the asm
+// barrier stops the compiler from folding the select back into x -- keeps
+// every division on the fast path.
+__device__ __forceinline__ double div_pos(double x, double y) {
+  const bool z = (x == 0.0);
+  double n = z ? 1.0 : x;
+  asm("mov.b64 %0, %0;" : "+d"(n));
+  const double q = n / y;
+  return z ? x : q;
+}
+
+// Free-road term (v / v0_eff)**delta (idm.py:24-25).
+__device__ __forceinline__ double idm_free(const Params& p, double v, double v0_eff) {
+  const double x = div_pos(v, v0_eff);
+  return p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
+}
+
+// idm.py:26-31 given the free term.  (s*/gap)**2 is the correctly rounded
+// square, i.e. q*q.
+// The interaction division is evaluated with a dummy divisor on a free road
+// (gap == inf): the compiler speculates it past the branch, and s*/inf == 0
+// would take the division slow path for every leaderless vehicle.
+__device__ __forceinline__ double idm_with_free(const Params& p, double fr, double v, double dv, double gap) {
+  const bool free_road = isinf(gap);
+  const double s_star = p.s0 + py_max(0.0, v * p.T + div_pos(v * dv, p.sqrt_ab2));
+  double g = free_road ? 1.0 : gap;
+  asm("mov.b64 %0, %0;" : "+d"(g));
+  const double q = div_pos(s_star, g);
+  const double inter = free_road ? 0.0 : q * q;
   return p.a_max * (1.0 - fr - inter);
+}
+
+// idm.py:17-31.
+__device__ __forceinline__ double idm_accel(const Params& p, double v, double dv, double gap, double v_cap) {
+  return idm_with_free(p, idm_free(p, v, py_min(p.v0, v_cap)), v, dv, gap);
 }
 
 // rng.py:24-41: splitmix64 finaliser fold over (seed, stream, id, step).

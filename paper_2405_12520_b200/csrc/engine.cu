@@ -174,9 +174,8 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_MISC, k_set_nc, 1, 1, c);
   LAUNCH(KC_SCATTER, k_scatter, vgrid, VB, c, SEL_B, &dy->n_a, nullptr, SEL_C, nullptr);
   LAUNCH(KC_LANESORT_SWEEP, k_lanesort<true>, wgrid, VB, c, SEL_C, nullptr);
-  LAUNCH(KC_RESOLVE, k_resolve_find, 148, 256, c);
-  LAUNCH(KC_RESOLVE, k_resolve_check, 296, 128, c);
-  LAUNCH(KC_RESOLVE, k_resolve_apply, 296, 128, c);
+  LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
+  LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
   if (c.p.controller == 1) {
     cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->stream);
@@ -252,12 +251,15 @@ static int set_route(tsb_engine* e, int32_t vix, const std::vector<int32_t>& roa
     cd.route_len = 0;
     cd.route_off = 0;
   } else {
-    RC(ensure_pool(e, (int64_t)roads.size()));
+    RC(ensure_pool(e, (int64_t)roads.size() + 1));
     cd.route_off = e->pool_used;
     cd.route_len = (int32_t)roads.size();
-    CK(cudaMemcpyAsync((int32_t*)e->c.routes + e->pool_used, roads.data(), sizeof(int32_t) * roads.size(),
+    std::vector<int32_t> buf(roads);
+    buf.push_back(-1);  // sentinel: "no next road" (see VRec::rptr)
+    CK(cudaMemcpyAsync((int32_t*)e->c.routes + e->pool_used, buf.data(), sizeof(int32_t) * buf.size(),
                        cudaMemcpyHostToDevice, e->stream));
-    e->pool_used += (int64_t)roads.size();
+    CK(cudaStreamSynchronize(e->stream));
+    e->pool_used += (int64_t)buf.size();
   }
   e->route_host[vix] = ok ? roads : std::vector<int32_t>();
   CK(cudaMemcpyAsync((VCold*)e->c.cold + vix, &cd, sizeof(VCold), cudaMemcpyHostToDevice, e->stream));
@@ -286,7 +288,7 @@ static int route_pending(tsb_engine* e, bool all) {
   std::vector<uint8_t> ok;
   e->router->route_batch(org, dst, roads, ok);
   int64_t need = 0;
-  for (size_t q = 0; q < idx.size(); q++) need += ok[q] ? (int64_t)roads[q].size() : 0;
+  for (size_t q = 0; q < idx.size(); q++) need += ok[q] ? (int64_t)roads[q].size() + 1 : 0;
   RC(ensure_pool(e, need));
   std::vector<int32_t> flat;
   flat.reserve(need);
@@ -296,6 +298,7 @@ static int route_pending(tsb_engine* e, bool all) {
       cd.route_off = e->pool_used + (int64_t)flat.size();
       cd.route_len = (int32_t)roads[q].size();
       flat.insert(flat.end(), roads[q].begin(), roads[q].end());
+      flat.push_back(-1);
       e->route_host[idx[q]] = std::move(roads[q]);
     } else {
       cd.route_off = 0;
@@ -303,6 +306,8 @@ static int route_pending(tsb_engine* e, bool all) {
       e->route_host[idx[q]].clear();
     }
   }
+  if ((int64_t)flat.size() + e->pool_used >= (int64_t)INT32_MAX)
+    return fail(TSB_ECAP, "route pool exceeds 2^31 entries");
   if (!flat.empty())
     CK(cudaMemcpy((int32_t*)e->c.routes + e->pool_used, flat.data(), sizeof(int32_t) * flat.size(),
                   cudaMemcpyHostToDevice));
@@ -340,7 +345,9 @@ static int host_continue(tsb_engine* e) {
     const int32_t i = q[k];
     VRec r;
     CK(cudaMemcpy(&r, e->c.B + i, sizeof(VRec), cudaMemcpyDeviceToHost));
-    int32_t lane = r.lane, rp = r.rp, vix = r.vix;
+    const int32_t vix = r.vix;
+    const int64_t off0 = e->cold[vix].route_off;
+    int32_t lane = r.lane, rp = (int32_t)(r.rptr - off0);
     double s = r.s, v = r.v;
     bool arrived = false;
     while (s > e->lanes[lane].len) {
@@ -395,12 +402,30 @@ static int host_continue(tsb_engine* e) {
       r.lane = lane;
       r.s = s;
       r.v = v;
-      r.rp = rp;
+      r.rptr = (int32_t)(e->cold[vix].route_off + rp);
     }
     CK(cudaMemcpy(e->c.B + i, &r, sizeof(VRec), cudaMemcpyHostToDevice));
+    const int64_t off1 = e->cold[vix].route_off;
+    if (off1 != off0) {
+      // rerouted: the snapshot record (revert target, world.py:501-507)
+      // keeps its road_pos but must point into the new roads_seq
+      VRec sn;
+      CK(cudaMemcpy(&sn, e->c.lay[d.cur] + i, sizeof(VRec), cudaMemcpyDeviceToHost));
+      sn.rptr = (int32_t)(off1 + (sn.rptr - off0));
+      CK(cudaMemcpy(e->c.lay[d.cur] + i, &sn, sizeof(VRec), cudaMemcpyHostToDevice));
+    }
   }
   d.finished_now = fin_now;
   CK(cudaMemcpy(&e->c.dyn->finished_now, &fin_now, sizeof(int64_t), cudaMemcpyHostToDevice));
+  return TSB_OK;
+}
+
+// Connector flag bits (signal aspect, successor open) from the current
+// junction states; run after construction and every control change.
+static int refresh_lane_flags(tsb_engine* e) {
+  if (e->n_junc > 0) k_lane_flags<<<grid_for(e->n_junc, 256, 148 * 4), 256, 0, e->stream>>>(e->c);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(e->stream));
   return TSB_OK;
 }
 
@@ -608,6 +633,16 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(upload(E, (int32_t**)&c.jc, jc.data(), jc.size()));
   RC(upload(E, &c.sig, sig.data(), NJ));
   RC(upload(E, (VCold**)&c.cold, e->cold.data(), N));
+  {
+    std::vector<uint64_t> keys(tr->key, tr->key + N);
+    c.ids_dense = 1;
+    for (int32_t k = 0; k < N; k++)
+      if (keys[k] != (uint64_t)k) c.ids_dense = 0;
+    RC(upload(E, (uint64_t**)&c.keys, keys.data(), N));
+    std::vector<uint8_t> lf(NL);
+    for (int32_t l = 0; l < NL; l++) lf[l] = net->lane_open[l] ? LF_OPEN : 0;
+    RC(upload(E, &c.lflag, lf.data(), NL));
+  }
   RC(upload(E, (int32_t**)&c.pend_vix, pend.data(), N));
   RC(upload(E, (double**)&c.pend_dep, pend_dep.data(), N));
   RC(dalloc(E, &c.status, N));
@@ -631,9 +666,14 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.scan_tiles, 1));
   RC(dalloc(E, &c.stage, (size_t)NL + 1));
   RC(dalloc(E, &c.events, NL));
-  RC(dalloc(E, &c.ev_x, NL));
-  RC(dalloc(E, &c.ev_lb, NL));
-  RC(dalloc(E, &c.tcount, NL));
+  RC(dalloc(E, &c.cl_idx, NL));
+  RC(dalloc(E, &c.cl_lanes, 2048));
+  RC(dalloc(E, &c.comp_id, 2048));
+  RC(dalloc(E, &c.comp_off, 2049));
+  RC(dalloc(E, &c.comp_size, 2048));
+  RC(dalloc(E, &c.comp_edges, 2048));
+  RC(dalloc(E, &c.comp_fill, 2048));
+  RC(dalloc(E, &c.comp_ev, 2048));
   RC(dalloc(E, &c.dirty_flag, NL));
   RC(dalloc(E, &c.dirty_list, NL));
   RC(dalloc(E, &c.patch_lanes, 4096));
@@ -681,6 +721,7 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   }
   RC(route_pending(E, true));
   RC(ensure_windows(E, 1));
+  RC(refresh_lane_flags(E));
   CK(cudaDeviceSynchronize());
   *out = e.release();
   return TSB_OK;
@@ -712,6 +753,7 @@ static void fill_report(const tsb_engine* e, tsb_report* r) {
   r->vehicle_updates = d.vehicle_updates;
   r->reverts_last = d.reverts_last;
   r->resolve_sequential = d.resolve_sequential;
+  r->reverts_total = d.reverts_total;
 }
 
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last) {
@@ -742,7 +784,7 @@ int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* v
   for (int32_t k = 0; k < n; k++) {
     if (vix) vix[k] = buf[k].vix;
     if (lane) lane[k] = buf[k].lane;
-    if (road_pos) road_pos[k] = buf[k].rp;
+    if (road_pos) road_pos[k] = (int32_t)(buf[k].rptr - e->cold[buf[k].vix].route_off);
     if (s) s[k] = buf[k].s;
     if (v) v[k] = buf[k].v;
   }
@@ -756,12 +798,14 @@ int tsb_status(tsb_engine* e, uint8_t* status, double* finish_time, int32_t* las
   if (finish_time) CK(cudaMemcpy(finish_time, e->c.finish, sizeof(double) * e->n_trips, cudaMemcpyDeviceToHost));
   if (last_lane || last_s || last_v || last_rp) {
     std::vector<VRec> fs(e->n_trips);
+    std::vector<uint8_t> st(e->n_trips);
+    CK(cudaMemcpy(st.data(), e->c.status, e->n_trips, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(fs.data(), e->c.fin_state, sizeof(VRec) * e->n_trips, cudaMemcpyDeviceToHost));
     for (int32_t k = 0; k < e->n_trips; k++) {
       if (last_lane) last_lane[k] = fs[k].lane;
       if (last_s) last_s[k] = fs[k].s;
       if (last_v) last_v[k] = fs[k].v;
-      if (last_rp) last_rp[k] = fs[k].rp;
+      if (last_rp) last_rp[k] = st[k] == TSB_STATUS_FINISHED ? (int32_t)(fs[k].rptr - e->cold[k].route_off) : 0;
     }
   }
   return TSB_OK;
@@ -822,6 +866,9 @@ int tsb_set_lane(tsb_engine* e, int32_t lane, double max_speed, int32_t open) {
   r.open = open ? 1 : 0;
   e->n_closed += (was_open && !r.open) ? 1 : (!was_open && r.open) ? -1 : 0;
   CK(cudaMemcpy((LaneRec*)e->c.lanes + lane, &r, sizeof(LaneRec), cudaMemcpyHostToDevice));
+  const uint8_t lf = r.open ? LF_OPEN : 0;
+  CK(cudaMemcpy(e->c.lflag + lane, &lf, 1, cudaMemcpyHostToDevice));
+  RC(refresh_lane_flags(e));
   e->router->set_lane(lane, max_speed, open != 0);
   e->routes_stale = true;  // router.rebuild(): routes not yet computed must use the new state
   return TSB_OK;
@@ -834,6 +881,7 @@ int tsb_set_signal_phase(tsb_engine* e, int32_t j, int32_t phase) {
     return fail(TSB_ERANGE, "phase index %d out of range (program has %d phases)", phase, np_);
   JuncState st{phase, 0, 0.0, 0.0};
   CK(cudaMemcpy(e->c.sig + j, &st, sizeof(JuncState), cudaMemcpyHostToDevice));
+  RC(refresh_lane_flags(e));
   return TSB_OK;
 }
 

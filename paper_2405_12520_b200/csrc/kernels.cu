@@ -67,19 +67,39 @@ __device__ __forceinline__ void mark_dirty(const Ctx& c, int32_t L) {
 // of road lane `lane` leading onto `road`.  Successor lists are sorted.
 __device__ __forceinline__ int32_t conn_from(const Ctx& c, const LaneRec& L, int32_t road) {
   for (int k = 0; k < L.nsucc; k++)
-    if (c.succ_dst_road[L.succ_off + k] == road) return c.succ[L.succ_off + k];
+    if (__ldg(c.succ_dst_road + L.succ_off + k) == road) return __ldg(c.succ + L.succ_off + k);
   return -1;
 }
 
-// world.py:247-254 + signals.py:46-61
-__device__ __forceinline__ int aspect(const Ctx& c, int32_t conn) {
-  int32_t j = c.lanes[conn].junc;
+__device__ __forceinline__ int lf_aspect(uint8_t f) { return (f >> LF_ASPECT_SHIFT) & 3; }
+// A connector a vehicle may enter: it and its successor lane are open
+// (world.py:282-283, 460-462).
+__device__ __forceinline__ bool lf_passable(uint8_t f) { return (f & (LF_OPEN | LF_SUCC_OPEN)) == (LF_OPEN | LF_SUCC_OPEN); }
+
+// Aspect of connector `conn` from its junction's state (world.py:247-254 +
+// signals.py:46-61).
+__device__ __forceinline__ int aspect_of(const Ctx& c, int32_t j, int32_t conn, const JuncState& st) {
   if (!c.junc_signal[j]) return GREEN;
-  JuncState st = c.sig[j];
   if (!((c.green[conn] >> st.phase) & 1ULL)) return RED;
   double dur = c.phase_dur[c.junc_phase_off[j] + st.phase];
   if (c.p.controller == 0 && c.p.amber > 0.0 && st.elapsed >= dur - c.p.amber) return AMBER;
   return GREEN;
+}
+
+// Refresh the connector bits of lflag for junction j's connectors.
+__device__ __forceinline__ void write_conn_flags(const Ctx& c, int32_t j, const JuncState& st) {
+  for (int32_t q = c.jc_off[j]; q < c.jc_off[j + 1]; q++) {
+    const int32_t cn = c.jc[q];
+    uint8_t f = c.lflag[cn] & LF_OPEN;
+    if (c.lflag[c.lanes[cn].succ1] & LF_OPEN) f |= LF_SUCC_OPEN;
+    f |= (uint8_t)(aspect_of(c, j, cn, st) << LF_ASPECT_SHIFT);
+    c.lflag[cn] = f;
+  }
+}
+
+// All junctions (after construction and after any host control change).
+__global__ void k_lane_flags(Ctx c) {
+  for (int32_t j = gtid(); j < c.n_junc; j += gstride()) write_conn_flags(c, j, c.sig[j]);
 }
 
 struct View {
@@ -92,49 +112,12 @@ __device__ __forceinline__ View view_at(const VRec* A, int32_t k) {
   return View{true, A[k].s, A[k].v};
 }
 
-// ------------------------------------------------------------------ MOBIL (mobil.py:33-98)
-
+// gap from follower position fs to leader l (mobil.py:33-36)
 __device__ __forceinline__ double gap_to(const View& l, double fs, double Lv) {
   return l.ok ? l.s - Lv - fs : CUDART_INF;
 }
-__device__ __forceinline__ double accel_behind(const Params& p, double me_v, const View& l, double gap, double cap) {
-  double dv = me_v - (l.ok ? l.v : 0.0);
-  return idm_accel(p, me_v, dv, gap, cap);
-}
-
-__device__ bool evaluate_change(const Params& p, View me, View cl, View cf, View tl, View tf, double s_t,
-                                double cap_cur, double cap_tgt, double& incentive) {
-  const double Lv = p.L;
-  double g_tl = gap_to(tl, s_t, Lv);
-  double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
-  if (g_tl <= 0.0 || g_tf <= 0.0) return false;
-  double g_cur = gap_to(cl, me.s, Lv);
-  double a_me = (g_cur <= 0.0) ? -CUDART_INF : accel_behind(p, me.v, cl, g_cur, cap_cur);
-  double a_me_new = accel_behind(p, me.v, tl, g_tl, cap_tgt);
-  double a_nf = 0.0, a_nf_new = 0.0;
-  if (tf.ok) {
-    double g_nf_old = gap_to(tl, tf.s, Lv);
-    if (g_nf_old <= 0.0) return false;
-    a_nf = accel_behind(p, tf.v, tl, g_nf_old, cap_tgt);
-    View mev{true, s_t, me.v};
-    a_nf_new = accel_behind(p, tf.v, mev, g_tf, cap_tgt);
-    if (a_nf_new < -p.b_safe) return false;
-  }
-  double a_of = 0.0, a_of_new = 0.0;
-  if (cf.ok) {
-    double g_of_old = me.s - Lv - cf.s;
-    double g_of_new = gap_to(cl, cf.s, Lv);
-    if (g_of_old > 0.0 && g_of_new > 0.0) {
-      a_of = accel_behind(p, cf.v, me, g_of_old, cap_cur);
-      a_of_new = accel_behind(p, cf.v, cl, g_of_new, cap_cur);
-    }
-  }
-  if (a_me == -CUDART_INF)
-    incentive = CUDART_INF;
-  else
-    incentive = (a_me_new - a_me) + p.politeness * ((a_nf_new - a_nf) + (a_of_new - a_of));
-  return true;
-}
+// speed difference to leader l, 0-speed stand-in when absent (mobil.py:39-42)
+__device__ __forceinline__ double dv_to(double v, const View& l) { return v - (l.ok ? l.v : 0.0); }
 
 // Number of records in A[lo, hi) strictly above s_t (world.py:325-330):
 // leader = lo+m-1, follower = lo+m.
@@ -165,8 +148,19 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
 
 // ------------------------------------------------------------------ k_update
 
-// World._update_vehicle + World._apply_deltas for one vehicle.
-__global__ void k_update(Ctx c) {
+// World._update_vehicle + World._apply_deltas for one vehicle (thread per
+// driving vehicle of the lane-sorted snapshot A; neighbours are adjacent
+// records, so a warp mostly covers one or two lanes).
+//
+// MOBIL (mobil.py:45-98, world.py:344-397) is restated with its pure
+// sub-terms shared instead of recomputed: the current-leader and
+// old-follower accelerations do not depend on the side evaluated, the
+// free-road term (v/v0_eff)^delta depends only on (v, v0_eff), and the
+// final IDM call of world.py:406 usually repeats one MOBIL already made
+// (same leader, same gap, same cap).  Every reused value is the same fp64
+// expression on the same operands, so results are bit-identical to the
+// per-call evaluation.
+__global__ void __launch_bounds__(256, 2) k_update(Ctx c) {
   Dyn* dy = c.dyn;
   const int32_t n = dy->n_a;
   const VRec* A = c.lay[dy->cur];
@@ -174,25 +168,32 @@ __global__ void k_update(Ctx c) {
   const Params& p = c.p;
   const uint64_t step_no = (uint64_t)dy->step_no;
   const double new_time = dy->time + p.dt;
+  const double Lv = p.L;
   for (int32_t i = gtid(); i < n; i += gstride()) {
     const VRec me = A[i];
     const int32_t snap_lane = me.lane;
     const LaneRec L0 = c.lanes[snap_lane];
-    const int32_t lo0 = S[snap_lane], hi0 = S[snap_lane + 1], pos = i - lo0;
-    const VCold cd = c.cold[me.vix];
-    const int32_t* roads = c.routes + cd.route_off;
-    const int32_t nroads = cd.route_len;
-    const int32_t rp = me.rp;
+    const int32_t lo0 = S[snap_lane], hi0 = S[snap_lane + 1];
+    const int32_t* roads = c.routes + me.rptr;  // roads[0] = current road, roads[1] = next (or -1)
+    const int32_t next_road = __ldg(roads + 1);
+    const double v = me.v;
+    const double v0e_cur = py_min(p.v0, L0.cap);
+
+    // Cached pure terms (valid flags below).
+    double fr_me = 0.0;  // free term of me at v0e_cur
+    bool have_fr_me = false;
+    double a_final = 0.0;
+    bool have_final = false;
 
     // ---- _consider_change (world.py:344-397)
     int32_t lane = snap_lane;
     double s = me.s;
-    const double v = me.v;
     bool changed = false;
+    int32_t best_tl = -1;       // target leader index of the chosen side
+    double best_a_new = 0.0, best_g_tl = 0.0;
     if (L0.kind == TSB_KIND_ROAD && (L0.left >= 0 || L0.right >= 0)) {
-      const bool any = rp + 1 >= nroads;
-      const int32_t nr = any ? -1 : roads[rp + 1];
-      const bool mandatory = !any && conn_from(c, L0, nr) < 0;
+      const bool any = next_road < 0;
+      const bool mandatory = !any && conn_from(c, L0, next_road) < 0;
       bool go = true;
       int32_t sides[2] = {L0.left, L0.right};
       int nsides = 2;
@@ -200,7 +201,7 @@ __global__ void k_update(Ctx c) {
         int32_t below = -1, above = -1;
         for (int32_t k = c.road_lane_off[L0.road]; k < c.road_lane_off[L0.road + 1]; k++) {
           int32_t f = c.road_lanes[k];
-          if (conn_from(c, c.lanes[f], nr) < 0) continue;
+          if (conn_from(c, c.lanes[f], next_road) < 0) continue;
           if (f < lane && (below < 0 || f > below)) below = f;
           if (f > lane && (above < 0 || f < above)) above = f;
         }
@@ -209,41 +210,103 @@ __global__ void k_update(Ctx c) {
         sides[0] = dl <= dr ? L0.left : L0.right;
         nsides = 1;
       } else {
-        double draw = keyed_uniform4(p.seed, 1ULL, cd.key, step_no);
+        const uint64_t key = c.ids_dense ? (uint64_t)me.vix : c.keys[me.vix];
+        double draw = keyed_uniform4(p.seed, 1ULL, key, step_no);
         go = !(draw >= p.eval_prob);
       }
       if (go) {
-        View mev{true, me.s, v};
-        View cl = view_at(A, pos > 0 ? i - 1 : -1);
-        View cf = view_at(A, i + 1 < hi0 ? i + 1 : -1);
+        const View mev{true, me.s, v};
+        const View cl = view_at(A, i > lo0 ? i - 1 : -1);
+        const View cf = view_at(A, i + 1 < hi0 ? i + 1 : -1);
+        // side-independent terms, computed on first use
+        bool have_common = false;
+        double a_me = 0.0, a_of = 0.0, a_of_new = 0.0;
+        const double g_cur = gap_to(cl, me.s, Lv);
         bool have = false;
         double best_inc = 0.0, best_s = 0.0;
         int32_t best_nb = -1;
         for (int k = 0; k < nsides; k++) {
-          int32_t nb = sides[k];
+          const int32_t nb = sides[k];
           if (nb < 0) continue;
+          if (!(c.lflag[nb] & LF_OPEN)) continue;
           const LaneRec LN = c.lanes[nb];
-          if (!LN.open) continue;
-          if (!mandatory && !any && conn_from(c, LN, nr) < 0) continue;
-          double s_t = me.s * (LN.len / L0.len);
-          int32_t lo = S[nb], hi = S[nb + 1];
-          int32_t m = count_above(A, lo, hi, s_t);
-          View tl = view_at(A, m > 0 ? lo + m - 1 : -1);
-          View tf = view_at(A, lo + m < hi ? lo + m : -1);
+          if (!mandatory && !any && conn_from(c, LN, next_road) < 0) continue;
+          const double s_t = me.s * (LN.len / L0.len);
+          const int32_t lo = S[nb], hi = S[nb + 1];
+          const int32_t m = count_above(A, lo, hi, s_t);
+          const int32_t tl_i = m > 0 ? lo + m - 1 : -1;
+          const View tl = view_at(A, tl_i);
+          const View tf = view_at(A, lo + m < hi ? lo + m : -1);
+          // ---- evaluate_change (mobil.py:45-98)
+          const double g_tl = gap_to(tl, s_t, Lv);
+          const double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
+          if (g_tl <= 0.0 || g_tf <= 0.0) continue;
+          if (!have_common) {
+            have_common = true;
+            if (!(g_cur <= 0.0)) {
+              fr_me = idm_free(p, v, v0e_cur);
+              have_fr_me = true;
+              a_me = idm_with_free(p, fr_me, v, dv_to(v, cl), g_cur);
+            } else {
+              a_me = -CUDART_INF;
+            }
+            if (cf.ok) {
+              const double g_of_old = me.s - Lv - cf.s;
+              const double g_of_new = gap_to(cl, cf.s, Lv);
+              if (g_of_old > 0.0 && g_of_new > 0.0) {
+                const double fr_cf = idm_free(p, cf.v, v0e_cur);
+                a_of = idm_with_free(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
+                a_of_new = idm_with_free(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
+              }
+            }
+          }
+          const double v0e_tgt = py_min(p.v0, LN.cap);
+          double fr_me_t;
+          if (have_fr_me && v0e_tgt == v0e_cur) {
+            fr_me_t = fr_me;
+          } else {
+            fr_me_t = idm_free(p, v, v0e_tgt);
+            if (v0e_tgt == v0e_cur) {
+              fr_me = fr_me_t;
+              have_fr_me = true;
+            }
+          }
+          const double a_me_new = idm_with_free(p, fr_me_t, v, dv_to(v, tl), g_tl);
+          double a_nf = 0.0, a_nf_new = 0.0;
+          if (tf.ok) {
+            const double g_nf_old = gap_to(tl, tf.s, Lv);
+            if (g_nf_old <= 0.0) continue;
+            const double fr_tf = idm_free(p, tf.v, v0e_tgt);
+            a_nf = idm_with_free(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
+            const View mt{true, s_t, v};
+            a_nf_new = idm_with_free(p, fr_tf, tf.v, dv_to(tf.v, mt), g_tf);
+            if (a_nf_new < -p.b_safe) continue;
+          }
           double inc;
-          if (!evaluate_change(p, mev, cl, cf, tl, tf, s_t, L0.cap, LN.cap, inc)) continue;
+          if (a_me == -CUDART_INF)
+            inc = CUDART_INF;
+          else
+            inc = (a_me_new - a_me) + p.politeness * ((a_nf_new - a_nf) + (a_of_new - a_of));
           if (!mandatory && inc <= p.threshold) continue;
           if (!have || inc > best_inc || (inc == best_inc && nb < best_nb)) {
             have = true;
             best_inc = inc;
             best_nb = nb;
             best_s = s_t;
+            best_tl = tl_i;
+            best_a_new = a_me_new;
+            best_g_tl = g_tl;
           }
         }
         if (have) {
           changed = true;
           lane = best_nb;
           s = best_s;
+        } else if (have_common && cl.ok && g_cur >= EPS_GAP) {
+          // world.py:406 will evaluate exactly a_me: same leader (i-1), gap
+          // max(g_cur, 1e-6) == g_cur, same cap
+          a_final = a_me;
+          have_final = true;
         }
       }
     }
@@ -252,37 +315,45 @@ __global__ void k_update(Ctx c) {
     const LaneRec L1 = changed ? c.lanes[lane] : L0;
     double gap = CUDART_INF, lead_v = 0.0;
     bool found = false;
-    {
+    if (!have_final) {
       int32_t lo = S[lane], hi = S[lane + 1];
       if (hi > lo) {
         int32_t ld = -1;
         if (!changed) {
-          if (pos > 0) ld = i - 1;
+          if (i > lo0) ld = i - 1;
         } else {
           int32_t m = count_ahead(A, lo, hi, s, me.vix);
           if (m > 0) ld = lo + m - 1;
         }
         if (ld >= 0) {
-          gap = py_max(A[ld].s - p.L - s, EPS_GAP);
-          lead_v = A[ld].v;
+          if (changed && ld == best_tl && best_g_tl >= EPS_GAP) {
+            a_final = best_a_new;  // MOBIL's a_me_new: same leader, gap, cap
+            have_final = true;
+          } else {
+            gap = py_max(A[ld].s - Lv - s, EPS_GAP);
+            lead_v = A[ld].v;
+          }
           found = true;
         }
       }
+    } else {
+      found = true;
     }
     if (!found) {
       const double remaining = L1.len - s;
       bool stop = false;
       if (L1.kind == TSB_KIND_ROAD) {
-        if (rp + 1 >= nroads) {
+        if (next_road < 0) {
           gap = CUDART_INF;
           lead_v = 0.0;
           found = true;
         } else {
-          int32_t conn = conn_from(c, L1, roads[rp + 1]);
-          if (conn < 0 || !c.lanes[conn].open || !c.lanes[c.lanes[conn].succ1].open) {
+          const int32_t conn = conn_from(c, L1, next_road);
+          const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
+          if (conn < 0 || !lf_passable(f)) {
             stop = true;
           } else {
-            int asp = aspect(c, conn);
+            const int asp = lf_aspect(f);
             if (asp == RED || (asp == AMBER && remaining > v * v / (2.0 * p.b))) stop = true;
           }
         }
@@ -293,7 +364,7 @@ __global__ void k_update(Ctx c) {
         }
       }
       if (!found) {
-        int32_t cur = lane, cur_rp = rp;
+        const int32_t* rq = roads;
         LaneRec LC = L1;
         double dist = remaining;
         gap = CUDART_INF;
@@ -301,58 +372,66 @@ __global__ void k_update(Ctx c) {
         while (dist < p.lookahead) {
           int32_t nxt;
           if (LC.kind == TSB_KIND_ROAD) {
-            nxt = (cur_rp + 1 >= nroads) ? -1 : conn_from(c, LC, roads[cur_rp + 1]);
-            if (nxt < 0 || !c.lanes[nxt].open) break;
+            const int32_t nr = __ldg(rq + 1);
+            nxt = nr < 0 ? -1 : conn_from(c, LC, nr);
+            if (nxt < 0 || !(c.lflag[nxt] & LF_OPEN)) break;
           } else {
             nxt = LC.succ1;
-            cur_rp += 1;
-            if (!c.lanes[nxt].open) break;
+            rq += 1;
+            if (!(c.lflag[nxt] & LF_OPEN)) break;
           }
-          int32_t lo = S[nxt], hi = S[nxt + 1];
+          const int32_t lo = S[nxt], hi = S[nxt + 1];
           if (hi > lo) {
             const VRec rear = A[hi - 1];
-            double g = dist + rear.s - p.L;
+            double g = dist + rear.s - Lv;
             gap = py_max(g, EPS_GAP);
             lead_v = rear.v;
             break;
           }
           LC = c.lanes[nxt];
           dist += LC.len;
-          cur = nxt;
         }
-        (void)cur;
       }
     }
 
     // ---- IDM + integration (world.py:406-419)
-    const double a = idm_accel(p, v, v - lead_v, gap, L1.cap);
+    double a;
+    if (have_final) {
+      a = a_final;
+    } else {
+      const double v0e = py_min(p.v0, L1.cap);
+      const double fr = (have_fr_me && v0e == v0e_cur) ? fr_me : idm_free(p, v, v0e);
+      a = idm_with_free(p, fr, v, v - lead_v, gap);
+    }
     const double dt = p.dt;
     double v_new = v + a * dt, disp;
     if (v_new <= 0.0) {
       v_new = 0.0;
-      disp = a < 0.0 ? v * v / (2.0 * -a) : 0.0;
+      disp = a < 0.0 ? div_pos(v * v, 2.0 * -a) : 0.0;
     } else {
       disp = v * dt + 0.5 * a * dt * dt;
       if (disp < 0.0) disp = 0.0;
     }
     double ns = s + disp, nv = v_new;
-    int32_t nl = lane, nrp = rp;
+    int32_t nl = lane, nptr = me.rptr;
 
     // ---- _apply_deltas transitions (world.py:443-499)
     LaneRec LT = L1;
     bool arrived = false, host = false;
     while (ns > LT.len) {
       if (LT.kind == TSB_KIND_ROAD) {
-        if (nrp + 1 >= nroads) {
+        const int32_t nr = __ldg(c.routes + nptr + 1);
+        if (nr < 0) {
           arrived = true;
           break;
         }
-        int32_t conn = conn_from(c, LT, roads[nrp + 1]);
-        if (conn >= 0 && (!c.lanes[conn].open || !c.lanes[c.lanes[conn].succ1].open)) {
+        const int32_t conn = conn_from(c, LT, nr);
+        const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
+        if (conn >= 0 && !lf_passable(f)) {
           host = true;  // reroute needs the host router (world.py:460-469)
           break;
         }
-        if (conn < 0 || aspect(c, conn) == RED) {
+        if (conn < 0 || lf_aspect(f) == RED) {
           ns = LT.len;
           nv = 0.0;
           break;
@@ -363,11 +442,11 @@ __global__ void k_update(Ctx c) {
       } else {
         ns -= LT.len;
         nl = LT.succ1;
-        nrp += 1;
+        nptr += 1;
         LT = c.lanes[nl];
       }
     }
-    VRec out{ns, nv, me.vix, nrp, nl, i};
+    VRec out{ns, nv, me.vix, nptr, nl, i};
     if (arrived) {
       out.lane = -1;
       c.status[me.vix] = TSB_STATUS_FINISHED;
@@ -612,245 +691,42 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
   }
 }
 
-// ------------------------------------------------------------------ resolve fast path
+// ------------------------------------------------------------------ revert resolution
 //
-// When every revert event is "simple" -- its lane La and target lane Lb are
-// touched by no other event, Lb is not itself an event lane, and neither the
-// re-sweep of La (without the reverted vehicle) nor the sweep of Lb (with it)
-// reverts again -- the reference's restart order reduces to independent
-// per-event work: events are processed in increasing lane order, so the
-// reach when event La reverts is exactly La, and Lb is restored to its
-// post-delta state iff Lb > La.  R1 finds each event's reverted vehicle,
-// R2 checks simplicity (any failure sets dyn->complex and the sequential
-// k_resolve replays everything from the untouched state), R3 applies.
+// k_lanesort's tentative sweep handles every lane whose sweep needs no
+// revert.  Lanes that would revert ("events") are resolved here by
+// replaying the reference's restart-after-revert loop (world.py:518-559)
+// exactly.  The replay only ever touches lanes reachable from an event lane
+// through "entered" vehicles: a revert moves an entered member of the lane
+// being swept (or its entered predecessor) back to its snapshot lane.
+// k_resolve_closure collects that closure and splits it into connected
+// components; k_resolve_comp replays each component in its own warp.
+//
+// Why components are independent (and exact): the reference's passes always
+// restart at lane 0 and stop at the smallest lane that reverts, so the lane
+// swept next is always the minimum pending lane -- a min-heap over dirty
+// lanes.  Components with disjoint lane sets interact only through "reach",
+// the largest lane any pass has swept, which decides whether a lane
+// receiving a reverted vehicle is swept for the first time (from its
+// post-delta state) or re-swept (from its clamped state).  When a component
+// X pops lane E, every lane popped by another component since X last popped
+// is < E (heap order), and before that < X's then-pending minimum, so the
+// global reach at any X event equals X's own reach.  If the closure does not
+// fit the on-chip budgets, the sequential k_resolve replays all events in
+// one warp instead (same algorithm, one global heap).
 
-struct SwM {
+static constexpr int RS_CAP = 192;     // members per lane staged on chip
+static constexpr int CL_CAP = 2048;    // closure lanes
+static constexpr int CE_CAP = 2048;    // closure edges (entered members)
+static constexpr int HCAP = 64;        // lanes per component (heap capacity)
+
+struct RsM {
   double s, v, snap_s;
-  int32_t j;        // index in C
-  int32_t vix;
-  uint8_t entered;  // lane != snapshot lane
-  uint8_t reverted;
-  uint8_t pad[2];
+  int32_t j, vix;
+  uint8_t entered, reverted, pad[6];
 };
-static constexpr int SW_CAP = 96;  // members per lane handled by the fast path
 
-// The reference's lane sweep (world.py:527-555) over m[0..n) sorted front
-// first; applies clamps/holds in place and returns the member to revert, or -1.
-__device__ int sweep_members(SwM* m, int n, const Params& p) {
-  int prev = -1;
-  double prev_rear = CUDART_INF;
-  for (int a = 0; a < n; a++) {
-    const double limit = prev_rear - p.s0_floor;
-    if (m[a].s > limit + 1e-12) {
-      const double floor_s = m[a].entered ? 0.0 : m[a].snap_s;
-      if (limit >= floor_s) {
-        m[a].v = py_max(0.0, py_min(m[a].v, m[a].v - (m[a].s - limit) / p.dt));
-        m[a].s = limit;
-      } else if (m[a].entered && !m[a].reverted) {
-        return a;
-      } else if (prev >= 0 && m[prev].entered && !m[prev].reverted) {
-        return prev;
-      } else {
-        m[a].v = 0.0;
-        m[a].s = floor_s;
-      }
-    }
-    prev = a;
-    prev_rear = m[a].s - p.L;
-  }
-  return -1;
-}
-
-// Load lane L's segment of C (entries still on L) into m; values from C or,
-// if `original`, from the post-delta B.  Returns count or -1 if over SW_CAP.
-__device__ int load_lane(const Ctx& c, const VRec* C, const int32_t* CS, const VRec* A, int32_t L, bool original,
-                         SwM* m) {
-  const int lane_id = threadIdx.x & 31;
-  const int32_t lo = CS[L], hi = CS[L + 1];
-  if (hi - lo > SW_CAP) return -1;
-  for (int32_t j = lo + lane_id; j < hi; j += 32) {
-    VRec r = C[j];
-    const VRec sn = A[r.src];
-    SwM x;
-    if (original) {
-      const VRec o = c.B[r.src];
-      x.s = o.s;
-      x.v = o.v;
-    } else {
-      x.s = r.s;
-      x.v = r.v;
-    }
-    x.snap_s = sn.s;
-    x.j = j;
-    x.vix = r.vix;
-    x.entered = r.lane != sn.lane;
-    x.reverted = 0;
-    m[j - lo] = x;
-  }
-  __syncwarp();
-  return hi - lo;
-}
-
-// Sort m[0..n) by (s desc, vix asc) with a warp rank sort through `tmp`.
-__device__ void sort_members(SwM* m, SwM* tmp, int n) {
-  const int lane_id = threadIdx.x & 31;
-  for (int a = lane_id; a < n; a += 32) tmp[a] = m[a];
-  __syncwarp();
-  for (int a = lane_id; a < n; a += 32) {
-    int rank = 0;
-    for (int b = 0; b < n; b++) rank += ahead_of(tmp[b].s, tmp[b].vix, tmp[a].s, tmp[a].vix) ? 1 : 0;
-    m[rank] = tmp[a];
-  }
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(256) k_resolve_find(Ctx c) {
-  __shared__ SwM sm[8][SW_CAP];
-  Dyn* dy = c.dyn;
-  const int ne = dy->n_events;
-  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  const VRec* C = c.lay[dy->cur ^ 1];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  const VRec* A = c.lay[dy->cur];
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
-    const int32_t La = c.events[e];
-    int n = load_lane(c, C, CS, A, La, false, sm[w]);
-    int32_t jx = -1, lb = -1;
-    if (n > 0 && lane_id == 0) {
-      int x = sweep_members(sm[w], n, c.p);
-      if (x >= 0) {
-        jx = sm[w][x].j;
-        lb = A[C[jx].src].lane;
-      }
-    }
-    if (lane_id == 0) {
-      c.ev_x[e] = jx;
-      c.ev_lb[e] = lb;
-      c.rs_event[La] = 1;
-      if (lb >= 0)
-        atomicAdd(&c.tcount[lb], 1);
-      if (lb < 0 || (c.debug & 1)) dy->complex = 1;  // oversized lane / forced: sequential path
-    }
-    __syncwarp();
-  }
-}
-
-// Simulates (apply=false) or applies (apply=true) one simple event.
-__device__ bool simple_event(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, int e, SwM* m, SwM* tmp,
-                             bool apply) {
-  const int lane_id = threadIdx.x & 31;
-  Dyn* dy = c.dyn;
-  const int32_t La = c.events[e], jx = c.ev_x[e], Lb = c.ev_lb[e];
-  // La: sweep to the revert, drop the reverted vehicle, re-sweep from the front
-  int n = load_lane(c, C, CS, A, La, false, m);
-  int ok = 1;
-  if (lane_id == 0) {
-    int x = sweep_members(m, n, c.p);
-    if (x < 0 || m[x].j != jx) ok = 0;
-    if (ok) {
-      for (int a = x; a + 1 < n; a++) m[a] = m[a + 1];
-      n -= 1;
-      if (sweep_members(m, n, c.p) >= 0) ok = 0;
-    }
-  }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  n = __shfl_sync(0xffffffffu, n, 0);
-  if (!ok) return false;
-  if (apply) {
-    for (int a = lane_id; a < n; a += 32) {
-      C[m[a].j].s = m[a].s;
-      C[m[a].j].v = m[a].v;
-    }
-  }
-  __syncwarp();
-  // Lb: its state when the reference sweeps it next, plus the reverted vehicle
-  int nb = load_lane(c, C, CS, A, Lb, Lb > La, m);
-  if (nb < 0 || nb + 1 > SW_CAP) return false;
-  const VRec rx = C[jx];
-  const VRec sx = A[rx.src];
-  if (lane_id == 0) {
-    SwM x;
-    x.s = sx.s;
-    x.v = 0.0;
-    x.snap_s = sx.s;
-    x.j = jx;
-    x.vix = rx.vix;
-    x.entered = 0;
-    x.reverted = 1;
-    m[nb] = x;
-  }
-  __syncwarp();
-  nb += 1;
-  sort_members(m, tmp, nb);
-  if (lane_id == 0) ok = sweep_members(m, nb, c.p) < 0;
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) return false;
-  if (apply) {
-    for (int a = lane_id; a < nb; a += 32) {
-      const int32_t j = m[a].j;
-      C[j].s = m[a].s;
-      C[j].v = m[a].v;
-    }
-    __syncwarp();
-    if (lane_id == 0) {
-      C[jx].lane = Lb;  // _revert (world.py:501-507); s, v set by the sweep above
-      C[jx].rp = sx.rp;
-      const int32_t q = atomicAdd(&dy->n_moved, 1);
-      c.rs_moved[q] = jx;
-      c.rs_movedin[Lb] = 1;
-      atomicAdd((unsigned long long*)&dy->reverts_last, 1ULL);
-      mark_dirty(c, La);
-      mark_dirty(c, Lb);
-    }
-  }
-  return true;
-}
-
-__global__ void __launch_bounds__(128) k_resolve_check(Ctx c) {
-  __shared__ SwM sm[4][SW_CAP];
-  __shared__ SwM tm[4][SW_CAP];
-  Dyn* dy = c.dyn;
-  const int ne = dy->n_events;
-  if (ne == 0 || dy->complex) return;
-  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  VRec* C = c.lay[dy->cur ^ 1];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  const VRec* A = c.lay[dy->cur];
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
-    const int32_t La = c.events[e], Lb = c.ev_lb[e];
-    bool ok = !c.rs_event[Lb] && c.tcount[Lb] == 1 && c.tcount[La] == 0;
-    if (ok) ok = simple_event(c, C, CS, A, e, sm[w], tm[w], false);
-    if (!ok && lane_id == 0) dy->complex = 1;
-    __syncwarp();
-  }
-}
-
-__global__ void __launch_bounds__(128) k_resolve_apply(Ctx c) {
-  __shared__ SwM sm[4][SW_CAP];
-  __shared__ SwM tm[4][SW_CAP];
-  Dyn* dy = c.dyn;
-  const int ne = dy->n_events;
-  if (ne == 0) return;
-  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  VRec* C = c.lay[dy->cur ^ 1];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  const VRec* A = c.lay[dy->cur];
-  const bool cx = dy->complex;
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += (gridDim.x * blockDim.x) >> 5) {
-    if (lane_id == 0) {
-      if (c.ev_lb[e] >= 0) c.tcount[c.ev_lb[e]] = 0;
-    }
-    if (!cx) {
-      simple_event(c, C, CS, A, e, sm[w], tm[w], true);
-      if (lane_id == 0) c.rs_event[c.events[e]] = 0;
-    }
-    __syncwarp();
-  }
-}
-
-// ------------------------------------------------------------------ resolve (exact revert chains)
-
-// Min-heap of lane ids in global scratch.
+// Min-heap of lane ids.
 __device__ void heap_push(int32_t* h, int32_t& n, int32_t x) {
   int32_t i = n++;
   h[i] = x;
@@ -880,68 +756,115 @@ __device__ int32_t heap_pop(int32_t* h, int32_t& n) {
   return top;
 }
 
-// Replays the reference's restart-after-revert sweep exactly, touching only
-// lanes involved in revert chains.  Lanes are
-// processed in the order the reference would next sweep them "for real":
-// always the smallest pending lane.  A lane that the reference has not yet
-// swept when it receives a reverted vehicle (id > reach) is first restored
-// to its post-delta state, because k_lanesort already applied its
-// tentative (membership-stale) sweep.
-__global__ void k_resolve(Ctx c) {
-  Dyn* dy = c.dyn;
-  const int32_t ne = dy->n_events;
-  if (ne == 0 || !dy->complex || threadIdx.x != 0 || blockIdx.x != 0) return;
-  dy->n_moved = 0;
-  dy->reverts_last = 0;
+// One lane of the replay, whole warp: gather the lane's current members (its
+// C segment entries still on it, plus vehicles reverted into it, listed in
+// moved[0, nmoved)), sort them (s desc, id asc), run the reference's sweep
+// (world.py:527-555) and write the clamped values back.  Returns the C index
+// of the vehicle to revert, or -1 (same value in every thread).
+__device__ int32_t resolve_lane(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, int32_t L,
+                                const int32_t* moved, int32_t nmoved, RsM* m, RsM* tmp) {
+  const int lid = threadIdx.x & 31;
   const Params& p = c.p;
-  VRec* C = c.lay[dy->cur ^ 1];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  const VRec* A = c.lay[dy->cur];
-  int32_t* heap = c.rs_heap;
-  int32_t hn = 0, nt = 0, nmoved = 0;
-  for (int32_t e = 0; e < ne; e++) {
-    int32_t L = c.events[e];
-    c.rs_event[L] = 1;
-    c.rs_inwork[L] = 1;
-    heap_push(heap, hn, L);
+  const int32_t lo = CS[L], hi = CS[L + 1];
+  int n = 0;
+  for (int32_t base = lo; base < hi; base += 32) {
+    const int32_t j = base + lid;
+    const bool mine = j < hi && C[j].lane == L;
+    const unsigned b = __ballot_sync(0xffffffffu, mine);
+    const int slot = n + __popc(b & ((1u << lid) - 1));
+    if (mine && slot < RS_CAP) {
+      const VRec r = C[j];
+      const VRec sn = A[r.src];
+      m[slot] = RsM{r.s, r.v, sn.s, j, r.vix, (uint8_t)(sn.lane != L), c.rs_reverted[j], {0}};
+    }
+    n += __popc(b);
   }
-  int32_t reach = -1;
-  int64_t reverts = 0;
-  const int64_t max_reverts = (int64_t)dy->n_c + 2;
-  while (hn > 0) {
-    const int32_t L = heap_pop(heap, hn);
-    if (!c.rs_inwork[L]) continue;
-    c.rs_inwork[L] = 0;
-    if (!c.rs_touched[L]) {
-      c.rs_touched[L] = 1;
-      c.rs_touched_list[nt++] = L;
-    }
-    if (L > reach) reach = L;
-    // members: segment entries still on L, plus vehicles reverted into L
-    int32_t m = 0;
-    for (int32_t j = CS[L]; j < CS[L + 1]; j++)
-      if (C[j].lane == L) c.rs_members[m++] = j;
-    if (c.rs_movedin[L])
-      for (int32_t q = 0; q < nmoved; q++) {
-        int32_t j = c.rs_moved[q];
-        if (C[j].lane == L && (j < CS[L] || j >= CS[L + 1])) c.rs_members[m++] = j;
+  if (c.rs_movedin[L]) {
+    for (int32_t base = 0; base < nmoved; base += 32) {
+      const int32_t q = base + lid;
+      int32_t j = -1;
+      if (q < nmoved) {
+        j = moved[q];
+        if (!(C[j].lane == L && (j < lo || j >= hi))) j = -1;
       }
-    // insertion sort by (s desc, vix asc)
-    for (int32_t a = 1; a < m; a++) {
-      int32_t x = c.rs_members[a];
-      int32_t b = a - 1;
-      while (b >= 0 && ahead_of(C[x].s, C[x].vix, C[c.rs_members[b]].s, C[c.rs_members[b]].vix)) {
-        c.rs_members[b + 1] = c.rs_members[b];
-        b--;
+      const unsigned b = __ballot_sync(0xffffffffu, j >= 0);
+      const int slot = n + __popc(b & ((1u << lid) - 1));
+      if (j >= 0 && slot < RS_CAP) {
+        const VRec r = C[j];
+        const VRec sn = A[r.src];
+        m[slot] = RsM{r.s, r.v, sn.s, j, r.vix, (uint8_t)(sn.lane != L), c.rs_reverted[j], {0}};
       }
-      c.rs_members[b + 1] = x;
+      n += __popc(b);
     }
-    // the reference's sweep of this lane (world.py:527-555)
+  }
+  __syncwarp();
+  int32_t rev = -1;
+  if (n <= RS_CAP) {
+    for (int a = lid; a < n; a += 32) tmp[a] = m[a];
+    __syncwarp();
+    for (int a = lid; a < n; a += 32) {
+      int rank = 0;
+      const double sa = tmp[a].s;
+      const int32_t va = tmp[a].vix;
+      for (int b2 = 0; b2 < n; b2++) rank += ahead_of(tmp[b2].s, tmp[b2].vix, sa, va) ? 1 : 0;
+      m[rank] = tmp[a];
+    }
+    __syncwarp();
+    if (lid == 0) {
+      int prev = -1;
+      double prev_rear = CUDART_INF;
+      for (int a = 0; a < n; a++) {
+        const double limit = prev_rear - p.s0_floor;
+        if (m[a].s > limit + 1e-12) {
+          const double floor_s = m[a].entered ? 0.0 : m[a].snap_s;
+          if (limit >= floor_s) {
+            m[a].v = py_max(0.0, py_min(m[a].v, m[a].v - (m[a].s - limit) / p.dt));
+            m[a].s = limit;
+          } else if (m[a].entered && !m[a].reverted) {
+            rev = m[a].j;
+            break;
+          } else if (prev >= 0 && m[prev].entered && !m[prev].reverted) {
+            rev = m[prev].j;
+            break;
+          } else {
+            m[a].v = 0.0;
+            m[a].s = floor_s;
+          }
+        }
+        prev = a;
+        prev_rear = m[a].s - p.L;
+      }
+    }
+    __syncwarp();
+    for (int a = lid; a < n; a += 32) {
+      C[m[a].j].s = m[a].s;
+      C[m[a].j].v = m[a].v;
+    }
+  } else if (lid == 0) {
+    // oversized lane (> RS_CAP members): sort indices in global scratch.
+    // Only the sequential replay gets here (k_resolve_closure sends any
+    // closure with an oversized lane to it), so one scratch array suffices.
+    int32_t* mem = c.rs_members;
+    int32_t cnt = 0;
+    for (int32_t j = lo; j < hi; j++)
+      if (C[j].lane == L) mem[cnt++] = j;
+    for (int32_t q = 0; q < nmoved; q++) {
+      const int32_t j = moved[q];
+      if (C[j].lane == L && (j < lo || j >= hi)) mem[cnt++] = j;
+    }
+    for (int32_t a = 1; a < cnt; a++) {
+      const int32_t x = mem[a];
+      int32_t b2 = a - 1;
+      while (b2 >= 0 && ahead_of(C[x].s, C[x].vix, C[mem[b2]].s, C[mem[b2]].vix)) {
+        mem[b2 + 1] = mem[b2];
+        b2--;
+      }
+      mem[b2 + 1] = x;
+    }
     int32_t prev = -1;
     double prev_rear = CUDART_INF;
-    int32_t rev = -1;
-    for (int32_t a = 0; a < m; a++) {
-      const int32_t j = c.rs_members[a];
+    for (int32_t a = 0; a < cnt; a++) {
+      const int32_t j = mem[a];
       VRec& r = C[j];
       const double limit = prev_rear - p.s0_floor;
       if (r.s > limit + 1e-12) {
@@ -965,60 +888,341 @@ __global__ void k_resolve(Ctx c) {
       prev = j;
       prev_rear = r.s - p.L;
     }
-    if (rev >= 0) {
-      reverts++;
+  }
+  rev = __shfl_sync(0xffffffffu, rev, 0);
+  __syncwarp();
+  return rev;
+}
+
+// State of one replay (a component, or everything in the sequential path).
+struct Replay {
+  int32_t* heap;
+  int32_t hn;
+  int32_t reach;
+  int32_t* moved;   // vehicles reverted so far (C indices)
+  int32_t nmoved;
+  int32_t* touched;  // lanes touched so far
+  int32_t nt;
+  int64_t reverts;
+};
+
+// Runs the min-heap replay until no pending lane reverts.  Lane 0 owns the
+// bookkeeping; the whole warp calls.  The heap must hold the initial lanes.
+__device__ void replay(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, Replay& R, RsM* m, RsM* tmp,
+                       int64_t max_reverts) {
+  const int lid = threadIdx.x & 31;
+  for (;;) {
+    int32_t L = -1;
+    if (lid == 0) {
+      while (R.hn > 0) {
+        const int32_t x = heap_pop(R.heap, R.hn);
+        if (!c.rs_inwork[x]) continue;
+        c.rs_inwork[x] = 0;
+        if (!c.rs_touched[x]) {
+          c.rs_touched[x] = 1;
+          R.touched[R.nt++] = x;
+        }
+        if (x > R.reach) R.reach = x;
+        L = x;
+        break;
+      }
+    }
+    L = __shfl_sync(0xffffffffu, L, 0);
+    if (L < 0) break;
+    const int32_t nmoved = __shfl_sync(0xffffffffu, R.nmoved, 0);
+    const int32_t rev = resolve_lane(c, C, CS, A, L, R.moved, nmoved, m, tmp);
+    if (rev < 0) continue;
+    // _revert (world.py:501-507) and rescheduling
+    const VRec sn = A[C[rev].src];
+    const int32_t Lb = sn.lane;
+    int restore = 0, stop = 0;
+    if (lid == 0) {
+      R.reverts++;
       VRec& r = C[rev];
-      const VRec sn = A[r.src];
-      const int32_t Lb = sn.lane;
-      const int32_t La = r.lane;
-      r.lane = sn.lane;  // _revert (world.py:501-507)
+      r.lane = sn.lane;
       r.s = sn.s;
       r.v = 0.0;
-      r.rp = sn.rp;
+      r.rptr = sn.rptr;
       c.rs_reverted[rev] = 1;
-      c.rs_moved[nmoved++] = rev;
+      R.moved[R.nmoved++] = rev;
       c.rs_movedin[Lb] = 1;
       if (!c.rs_touched[Lb]) {
         c.rs_touched[Lb] = 1;
-        c.rs_touched_list[nt++] = Lb;
-        if (Lb > reach && !c.rs_event[Lb]) {
-          // undo k_lanesort's tentative sweep: the reference sweeps Lb for
-          // the first time only now, with the reverted vehicle present
-          for (int32_t j = CS[Lb]; j < CS[Lb + 1]; j++) {
-            const VRec o = c.B[C[j].src];
-            C[j].s = o.s;
-            C[j].v = o.v;
-          }
-        }
+        R.touched[R.nt++] = Lb;
+        // the reference sweeps Lb for the first time only now, with the
+        // reverted vehicle present: undo k_lanesort's tentative sweep
+        restore = (Lb > R.reach && !c.rs_event[Lb]) ? 1 : 0;
       }
-      if (!c.rs_inwork[La]) {
-        c.rs_inwork[La] = 1;
-        heap_push(heap, hn, La);
+      if (!c.rs_inwork[L]) {
+        c.rs_inwork[L] = 1;
+        heap_push(R.heap, R.hn, L);
       }
       if (!c.rs_inwork[Lb]) {
         c.rs_inwork[Lb] = 1;
-        heap_push(heap, hn, Lb);
+        heap_push(R.heap, R.hn, Lb);
       }
-      if (reverts >= max_reverts) break;  // the reference's pass bound (world.py:518)
+      stop = R.reverts >= max_reverts;  // the reference's pass bound (world.py:518)
     }
+    restore = __shfl_sync(0xffffffffu, restore, 0);
+    if (restore)
+      for (int32_t j = CS[Lb] + lid; j < CS[Lb + 1]; j += 32) {
+        const VRec o = c.B[C[j].src];
+        C[j].s = o.s;
+        C[j].v = o.v;
+      }
+    __syncwarp();
+    if (__shfl_sync(0xffffffffu, stop, 0)) break;
   }
-  // clear scratch; every touched lane is rebuilt in the next snapshot
-  for (int32_t q = 0; q < nt; q++) mark_dirty(c, c.rs_touched_list[q]);
-  for (int32_t q = 0; q < nt; q++) {
-    int32_t L = c.rs_touched_list[q];
+}
+
+// Clears the per-lane replay flags of R's lanes and marks them dirty (their
+// membership or order changed: the next snapshot rebuilds them).
+__device__ void replay_finish(const Ctx& c, const Replay& R) {
+  for (int32_t q = 0; q < R.nt; q++) {
+    const int32_t L = R.touched[q];
+    mark_dirty(c, L);
     c.rs_touched[L] = 0;
     c.rs_event[L] = 0;
     c.rs_movedin[L] = 0;
     c.rs_inwork[L] = 0;
   }
-  for (int32_t e = 0; e < ne; e++) {
-    c.rs_event[c.events[e]] = 0;
-    c.rs_inwork[c.events[e]] = 0;
+  for (int32_t q = 0; q < R.nmoved; q++) c.rs_reverted[R.moved[q]] = 0;
+}
+
+// Closure of the event lanes under "entered member -> its snapshot lane",
+// split into components (one CTA).  Output: dy->n_comp components, comp_off
+// / comp_ev (event lanes per component), comp_size; or dy->complex = 1 when
+// a budget is exceeded (then the sequential replay runs instead).
+__global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
+  Dyn* dy = c.dyn;
+  __shared__ int32_t cl[CL_CAP];
+  __shared__ int32_t lab[CL_CAP];
+  __shared__ int32_t eu[CE_CAP], ev[CE_CAP];
+  __shared__ int32_t indeg[CL_CAP];
+  __shared__ int32_t s_n, s_ne, s_over, s_changed, s_ncomp;
+  const int32_t ne = dy->n_events;
+  // clear the previous step's closure marks
+  for (int32_t q = threadIdx.x; q < dy->n_cl; q += blockDim.x) c.cl_idx[c.cl_lanes[q]] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dy->n_cl = 0;
+    dy->n_comp = 0;
+    s_n = 0;
+    s_ne = 0;
+    s_over = (ne > CL_CAP) || (c.debug & 1);
   }
-  for (int32_t q = 0; q < nmoved; q++) c.rs_reverted[c.rs_moved[q]] = 0;
-  dy->n_moved = nmoved;
-  dy->reverts_last = reverts;
-  dy->resolve_sequential += 1;
+  __syncthreads();
+  if (ne == 0 || s_over) {
+    if (threadIdx.x == 0 && ne > 0) dy->complex = 1;
+    return;
+  }
+  for (int32_t e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int32_t L = c.events[e];
+    cl[e] = L;
+    c.cl_idx[L] = e + 1;
+    c.rs_event[L] = 1;
+  }
+  if (threadIdx.x == 0) s_n = ne;
+  __syncthreads();
+  const VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  const int w = threadIdx.x >> 5, lid = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int32_t f_lo = 0, f_hi = ne;
+  while (f_lo < f_hi) {
+    for (int32_t i = f_lo + w; i < f_hi; i += nw) {
+      const int32_t L = cl[i];
+      for (int32_t j = CS[L] + lid; j < CS[L + 1]; j += 32) {
+        const VRec r = C[j];
+        const int32_t T = A[r.src].lane;
+        if (T == L) continue;  // not entered
+        const int32_t k = atomicAdd(&s_ne, 1);
+        if (k < CE_CAP) {
+          eu[k] = L;
+          ev[k] = T;
+        }
+        if (atomicCAS(&c.cl_idx[T], 0, -1) == 0) {
+          const int32_t x = atomicAdd(&s_n, 1);
+          if (x < CL_CAP) {
+            cl[x] = T;
+            c.cl_idx[T] = x + 1;
+          } else {
+            c.cl_idx[T] = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_n > CL_CAP || s_ne > CE_CAP) break;
+    f_lo = f_hi;
+    f_hi = s_n;
+    __syncthreads();
+  }
+  const int32_t n = min(s_n, CL_CAP), nedge = min(s_ne, CE_CAP);
+  if (threadIdx.x == 0) s_over = s_n > CL_CAP || s_ne > CE_CAP;
+  // record the closure for clearing (next step)
+  for (int32_t q = threadIdx.x; q < n; q += blockDim.x) c.cl_lanes[q] = cl[q];
+  if (threadIdx.x == 0) dy->n_cl = n;
+  __syncthreads();
+  if (s_over) {
+    if (threadIdx.x == 0) dy->complex = 1;
+    return;
+  }
+  // on-chip budget per lane: members now + vehicles that can be reverted into it
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) indeg[i] = 0;
+  __syncthreads();
+  for (int32_t k = threadIdx.x; k < nedge; k += blockDim.x) atomicAdd(&indeg[c.cl_idx[ev[k]] - 1], 1);
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
+    if (CS[cl[i] + 1] - CS[cl[i]] + indeg[i] > RS_CAP) s_over = 1;
+  __syncthreads();
+  if (s_over) {
+    if (threadIdx.x == 0) dy->complex = 1;
+    return;
+  }
+  // connected components: min-label propagation with pointer jumping
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) lab[i] = i;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_changed = 0;
+    __syncthreads();
+    for (int32_t k = threadIdx.x; k < nedge; k += blockDim.x) {
+      const int32_t a = c.cl_idx[eu[k]] - 1, b = c.cl_idx[ev[k]] - 1;
+      const int32_t la = lab[a], lb = lab[b];
+      if (la != lb) {
+        const int32_t mn = min(la, lb);
+        atomicMin(&lab[a], mn);
+        atomicMin(&lab[b], mn);
+        atomicMin(&lab[la], mn);
+        atomicMin(&lab[lb], mn);
+        s_changed = 1;
+      }
+    }
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      int32_t x = lab[i];
+      while (lab[x] != x) x = lab[x];
+      lab[i] = x;
+    }
+    __syncthreads();
+    if (!s_changed) break;
+    __syncthreads();
+  }
+  // component ids (roots in index order), sizes, events per component
+  if (threadIdx.x == 0) {
+    int32_t nc = 0;
+    for (int32_t i = 0; i < n; i++)
+      if (lab[i] == i) c.comp_id[i] = nc++;
+    s_ncomp = nc;
+    for (int32_t k = 0; k <= nc; k++) c.comp_off[k] = 0;
+  }
+  __syncthreads();
+  const int32_t nc = s_ncomp;
+  for (int32_t k = threadIdx.x; k < nc; k += blockDim.x) {
+    c.comp_size[k] = 0;
+    c.comp_edges[k] = 0;
+  }
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int32_t k = c.comp_id[lab[i]];
+    atomicAdd(&c.comp_size[k], 1);
+    if (i < ne) atomicAdd(&c.comp_off[k + 1], 1);
+  }
+  for (int32_t e = threadIdx.x; e < nedge; e += blockDim.x)
+    atomicAdd(&c.comp_edges[c.comp_id[lab[c.cl_idx[eu[e]] - 1]]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int32_t k = 0; k < nc; k++) {
+      c.comp_off[k + 1] += c.comp_off[k];
+      // heap / touched lists hold distinct lanes; each revert moves a
+      // distinct entered member (an edge)
+      if (c.comp_size[k] > HCAP || c.comp_edges[k] > 2 * HCAP) s_over = 1;
+    }
+    for (int32_t k = 0; k < nc; k++) c.comp_fill[k] = c.comp_off[k];
+  }
+  __syncthreads();
+  if (s_over) {
+    if (threadIdx.x == 0) dy->complex = 1;
+    return;
+  }
+  for (int32_t i = threadIdx.x; i < ne; i += blockDim.x) {
+    const int32_t k = c.comp_id[lab[i]];
+    c.comp_ev[atomicAdd(&c.comp_fill[k], 1)] = cl[i];
+  }
+  if (threadIdx.x == 0) dy->n_comp = nc;
+}
+
+// One warp per component: the replay restricted to the component's lanes.
+static constexpr int RC_WARPS = 2;
+__global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t nc = dy->n_comp;
+  if (nc == 0 || dy->complex) return;
+  __shared__ RsM sm[RC_WARPS][RS_CAP];
+  __shared__ RsM st[RC_WARPS][RS_CAP];
+  __shared__ int32_t sh[RC_WARPS][HCAP], smv[RC_WARPS][2 * HCAP], stl[RC_WARPS][HCAP];
+  const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  const int64_t max_reverts = (int64_t)dy->n_c + 2;
+  for (int32_t k = blockIdx.x * RC_WARPS + w; k < nc; k += gridDim.x * RC_WARPS) {
+    Replay R{sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
+    if (lid == 0)
+      for (int32_t q = c.comp_off[k]; q < c.comp_off[k + 1]; q++) {
+        const int32_t L = c.comp_ev[q];
+        c.rs_inwork[L] = 1;
+        heap_push(R.heap, R.hn, L);
+      }
+    __syncwarp();
+    // heap / touched <= HCAP lanes and moved <= 2 * HCAP vehicles
+    // (component budgets checked by k_resolve_closure)
+    replay(c, C, CS, A, R, sm[w], st[w], max_reverts);
+    if (lid == 0) {
+      replay_finish(c, R);
+      const int32_t base = atomicAdd(&dy->n_moved, R.nmoved);
+      for (int32_t q = 0; q < R.nmoved; q++) c.rs_moved[base + q] = R.moved[q];
+      atomicAdd((unsigned long long*)&dy->reverts_last, (unsigned long long)R.reverts);
+    }
+    __syncwarp();
+  }
+}
+
+// Sequential replay of all events (fallback when the closure exceeds the
+// component budgets, or forced by the debug knob).
+__global__ void __launch_bounds__(32) k_resolve(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t ne = dy->n_events;
+  if (ne == 0 || !dy->complex) return;
+  __shared__ RsM m[RS_CAP];
+  __shared__ RsM tmp[RS_CAP];
+  const int lid = threadIdx.x;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  Replay R{c.rs_heap, 0, -1, c.rs_moved, 0, c.rs_touched_list, 0, 0};
+  if (lid == 0) {
+    dy->n_moved = 0;
+    dy->reverts_last = 0;
+    for (int32_t e = 0; e < ne; e++) {
+      const int32_t L = c.events[e];
+      c.rs_event[L] = 1;
+      c.rs_inwork[L] = 1;
+      heap_push(R.heap, R.hn, L);
+    }
+  }
+  __syncwarp();
+  replay(c, C, CS, A, R, m, tmp, (int64_t)dy->n_c + 2);
+  if (lid == 0) {
+    replay_finish(c, R);
+    for (int32_t e = 0; e < ne; e++) {
+      c.rs_event[c.events[e]] = 0;
+      c.rs_inwork[c.events[e]] = 0;
+    }
+    dy->n_moved = R.nmoved;
+    dy->reverts_last = R.reverts;
+    dy->resolve_sequential += 1;
+  }
 }
 
 // ------------------------------------------------------------------ signals + clock
@@ -1074,6 +1278,7 @@ __global__ void k_signals(Ctx c) {
       }
     }
     c.sig[j] = st;
+    write_conn_flags(c, j, st);
   }
 }
 
@@ -1150,7 +1355,7 @@ __global__ void k_inject_lanes(Ctx c) {
       }
       c.due_grp[b + 1] = x;
     }
-    const bool lane_open = c.lanes[L].open;
+    const bool lane_open = c.lflag[L] & LF_OPEN;
     for (int32_t q = lo; q < hi; q++) {
       const int32_t dpos = c.due_grp[q];
       const int32_t vx = c.due[dpos];
@@ -1193,7 +1398,7 @@ __global__ void k_inject_lanes(Ctx c) {
         } else {
           outc = OUT_INJECT;
           int32_t k = atomicAdd(&dy->n_inj, 1);
-          VRec nr_{o_s, 0.0, vx, 0, L, -1};
+          VRec nr_{o_s, 0.0, vx, (int32_t)cd.route_off, L, -1};
           C[dy->n_c + k] = nr_;
           c.status[vx] = TSB_STATUS_DRIVING;
           mark_dirty(c, L);
@@ -1428,6 +1633,7 @@ __global__ void k_speeds(Ctx c) {
 __global__ void k_end_step(Ctx c) {
   Dyn* dy = c.dyn;
   dy->finished_total += dy->finished_now;
+  dy->reverts_total += dy->reverts_last;
   dy->fin_log_n += dy->finished_now;
 }
 
