@@ -14,7 +14,9 @@ from .cabi import TsbReport
 from .errors import EngineError, InputError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsb200.so")
+# TSB200_LIB lets kernel experiments load an alternative in-tree build of the
+# same C-ABI (default: the library `__graft_entry__.build()` makes).
+LIB_PATH = os.environ.get("TSB200_LIB") or os.path.join(HERE, "libtsb200.so")
 
 TSB_EINVAL, TSB_ERANGE = -1, -2
 

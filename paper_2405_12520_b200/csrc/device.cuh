@@ -156,9 +156,16 @@ struct Ctx {
   VRec* D;
   int32_t* cnt;
   int32_t* cursor;
-  unsigned long long* scan_status;
-  int32_t* scan_tiles;
+  unsigned long long* scan_status;   // SCAN_SITES regions of scan_tiles_cap words
+  unsigned long long* scan_tickets;  // per scan site, never reset
   int32_t scan_tiles_cap;
+  // conditional sections of the step graph (kernels.cu set_cond)
+  unsigned long long cond[4];
+  int32_t use_cond;
+  // connectors in junction order (jc) with their junction / successor lane
+  int32_t n_conn;
+  const int32_t* jc_junc;
+  const int32_t* jc_succ1;
   int32_t* stage;  // scan staging (n_lanes + 1)
   int32_t* events;
   // revert closure / components (k_resolve_closure)
@@ -278,6 +285,13 @@ __device__ __forceinline__ double idm_with_free(const Params& p, double fr, doub
   const double q = div_pos(s_star, g);
   const double inter = free_road ? 0.0 : q * q;
   return p.a_max * (1.0 - fr - inter);
+}
+
+// idm_with_free for a gap that may be <= 0 where the caller discards the
+// result (branch-free MOBIL evaluation): a safe divisor keeps the division
+// on its fast path; for gap > 0 it is the same expression, bit for bit.
+__device__ __forceinline__ double idm_safe(const Params& p, double fr, double v, double dv, double gap) {
+  return idm_with_free(p, fr, v, dv, gap > 0.0 ? gap : 1.0);
 }
 
 // idm.py:17-31.

@@ -84,6 +84,11 @@ struct tsb_engine {
   bool graph_dirty = true;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cur = nullptr;   // launch stream (see LAUNCH)
+  cudaStream_t body = nullptr;  // captures conditional-section bodies
+  cudaGraph_t body_graph = nullptr;
+  bool capturing = false;
+  cudaError_t capture_err = cudaSuccess;
   int32_t launches_per_step = 0;
   // profiling
   bool profiling = false;
@@ -134,20 +139,53 @@ struct Launcher {
   }
 };
 
-#define LAUNCH(kc, kern, grid, block, ...)                  \
-  do {                                                      \
-    L.pre(kc);                                              \
-    kern<<<(grid), (block), 0, e->stream>>>(__VA_ARGS__);  \
-    L.post();                                               \
+// Kernels go to e->cur: the engine stream, or while a conditional section is
+// being captured, the stream capturing its body graph.
+#define LAUNCH(kc, kern, grid, block, ...)                \
+  do {                                                    \
+    L.pre(kc);                                            \
+    kern<<<(grid), (block), 0, e->cur>>>(__VA_ARGS__);   \
+    L.post();                                             \
   } while (0)
 
-static void scan(tsb_engine* e, Launcher& L, int kc, const int32_t* in, int32_t* out, int out_sel,
+static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in, int32_t* out, int out_sel,
                  const int32_t* n_dev, int32_t n_static, int64_t n_max, const int32_t* gate) {
   Ctx& c = e->c;
-  cudaMemsetAsync(c.scan_status, 0, sizeof(unsigned long long) * c.scan_tiles_cap, e->stream);
-  cudaMemsetAsync(c.scan_tiles, 0, sizeof(int32_t), e->stream);
-  int grid = (int)(n_max / SCAN_TILE + 1);
-  LAUNCH(kc, (k_scan<SCAN_BT, SCAN_IPT>), grid, SCAN_BT, c, in, out, out_sel, n_dev, n_static, gate);
+  const int ntiles = (int)(n_max / SCAN_TILE + 1);
+  LAUNCH(kc, (k_scan<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, site, in, out, out_sel, n_dev, n_static, ntiles, gate);
+}
+
+// Conditional section (graph capture only): an IF node on handle c.cond[k]
+// whose body captures every launch until cond_end.  Outside capture both are
+// no-ops and the section's kernels gate themselves on the same flags.
+static void cond_begin(tsb_engine* e, int k) {
+  if (!e->capturing) return;
+  cudaStreamCaptureStatus st;
+  unsigned long long id;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps;
+  size_t nd;
+  cudaError_t er = cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd);
+  cudaGraphNodeParams prm = {};
+  prm.type = cudaGraphNodeTypeConditional;
+  prm.conditional.handle = e->c.cond[k];
+  prm.conditional.type = cudaGraphCondTypeIf;
+  prm.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (er == cudaSuccess) er = cudaGraphAddNode(&node, g, deps, nd, &prm);
+  if (er == cudaSuccess) er = cudaStreamUpdateCaptureDependencies(e->stream, &node, 1, cudaStreamSetCaptureDependencies);
+  if (er == cudaSuccess) {
+    e->body_graph = prm.conditional.phGraph_out[0];
+    er = cudaStreamBeginCaptureToGraph(e->body, e->body_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  }
+  if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
+  e->cur = e->body;
+}
+static void cond_end(tsb_engine* e) {
+  if (!e->capturing) return;
+  cudaError_t er = cudaStreamEndCapture(e->body, &e->body_graph);
+  if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
+  e->cur = e->stream;
 }
 
 // phase 0 = whole step; 1 = through k_update; 2 = the rest (split mode).
@@ -160,58 +198,59 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   const int rgrid = grid_for((int64_t)e->n_roads * 32, VB, 148 * 16);
   const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
   const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
+  const int cgrid = grid_for(std::max(c.n_conn, 1), VB, 148 * 8);
   const int32_t NL = e->n_lanes;
   if (phase != 2) {
     LAUNCH(KC_MISC, k_begin_step, 1, 1, c);
-    cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->stream);
-    cudaMemsetAsync(c.cursor, 0, sizeof(int32_t) * NL, e->stream);
-    LAUNCH(KC_UPDATE, k_update, vgrid, VB, c);
+    LAUNCH(KC_UPDATE, k_update, grid_for(e->n_trips, UPD_BT, 148 * 2048 / UPD_BT), UPD_BT, c);
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
   // bucket the post-delta state by lane, sort each lane, tentative sweep
-  scan(e, L, KC_SCAN, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
-  LAUNCH(KC_MISC, k_set_nc, 1, 1, c);
+  scan(e, L, KC_SCAN, SCAN_LANES, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
   LAUNCH(KC_SCATTER, k_scatter, vgrid, VB, c, SEL_B, &dy->n_a, nullptr, SEL_C, nullptr);
   LAUNCH(KC_LANESORT_SWEEP, k_lanesort<true>, wgrid, VB, c, SEL_C, nullptr);
+  // exact revert resolution (only when some lane's sweep reverts)
   LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
+  cond_begin(e, COND_RESOLVE);
   LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
+  cond_end(e);
   if (c.p.controller == 1) {
-    cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->stream);
+    cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->cur);
     LAUNCH(KC_SIGNALS, k_lane_counts, vgrid, VB, c);
   }
   LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
-  LAUNCH(KC_MISC, k_clock, 1, 1, c);
-  // injection
-  cudaMemsetAsync(c.inj_cnt, 0, sizeof(int32_t) * NL, e->stream);
-  cudaMemsetAsync(c.inj_cursor, 0, sizeof(int32_t) * NL, e->stream);
+  LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+  // injection (only when trips are due or waiting for a retry)
   LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
+  cond_begin(e, COND_INJECT);
   LAUNCH(KC_INJECT, k_inject_hist, vgrid, VB, c);
-  scan(e, L, KC_INJECT, c.inj_cnt, c.inj_start, SEL_NONE, nullptr, NL, NL, &dy->n_due);
+  scan(e, L, KC_INJECT, SCAN_INJ_LANES, c.inj_cnt, c.inj_start, SEL_NONE, nullptr, NL, NL, &dy->n_due);
   LAUNCH(KC_INJECT, k_inject_scatter, vgrid, VB, c);
   LAUNCH(KC_INJECT, k_inject_lanes, tgrid, VB, c);
   LAUNCH(KC_INJECT, k_retry_flags, vgrid, VB, c);
-  scan(e, L, KC_INJECT, c.flag_in, c.flag_scan, SEL_NONE, &dy->n_due, 0, e->n_trips, &dy->n_due);
+  scan(e, L, KC_INJECT, SCAN_INJ_RETRY, c.flag_in, c.flag_scan, SEL_NONE, &dy->n_due, 0, e->n_trips, &dy->n_due);
   LAUNCH(KC_INJECT, k_retry_compact, vgrid, VB, c);
   LAUNCH(KC_INJECT, k_inject_finish, 1, 1, c);
+  cond_end(e);
   // next snapshot: nothing if no lane changed membership/order; else rebuild
   // only the dirty lanes and shift the rest; full regroup if too many changed
   LAUNCH(KC_REGROUP, k_patch_prepare, 1, 1024, c);
+  cond_begin(e, COND_PATCH);
   LAUNCH(KC_REGROUP, k_patch_starts, tgrid, VB, c);
   LAUNCH(KC_REGROUP, k_patch_copy, vgrid, VB, c);
   LAUNCH(KC_REGROUP, k_patch_dirty, 64, VB, c);
-  cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->stream);
-  cudaMemsetAsync(c.cursor, 0, sizeof(int32_t) * NL, e->stream);
+  cond_end(e);
+  cond_begin(e, COND_FULL);
   LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->full_regroup);
-  scan(e, L, KC_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->full_regroup);
+  scan(e, L, KC_REGROUP, SCAN_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
+  cond_end(e);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
-  LAUNCH(KC_MISC, k_commit_layout, 1, 1, c);
   LAUNCH(KC_SPEEDS, k_speeds, rgrid, VB, c);
-  LAUNCH(KC_MISC, k_end_step, 1, 1, c);
 }
 
 // ----------------------------------------------------------------- host side pieces
@@ -464,8 +503,26 @@ static int build_graph(tsb_engine* e) {
     e->graph = nullptr;
   }
   CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+  {
+    cudaStreamCaptureStatus st;
+    unsigned long long id;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps;
+    size_t nd;
+    CK(cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd));
+    for (int k = 0; k < N_COND; k++)
+      CK(cudaGraphConditionalHandleCreate((cudaGraphConditionalHandle*)&e->c.cond[k], g, 0,
+                                          cudaGraphCondAssignDefault));
+  }
+  e->c.use_cond = 1;
+  e->capturing = true;
+  e->capture_err = cudaSuccess;
   Launcher L{e};
   issue_step(e, L, 0);
+  e->capturing = false;
+  e->c.use_cond = 0;
+  e->cur = e->stream;
+  CK(e->capture_err);
   CK(cudaStreamEndCapture(e->stream, &e->graph));
   CK(cudaGraphInstantiate(&e->gexec, e->graph, 0));
   e->launches_per_step = L.count;
@@ -515,6 +572,8 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   e->device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->body, cudaStreamNonBlocking));
+  e->cur = e->stream;
   const int32_t NL = e->n_lanes = net->n_lanes;
   const int32_t NR = e->n_roads = net->n_roads;
   const int32_t NJ = e->n_junc = net->n_junctions;
@@ -631,6 +690,16 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(upload(E, (uint8_t**)&c.junc_signal, net->junc_signal, NJ));
   RC(upload(E, (int32_t**)&c.jc_off, jc_off.data(), NJ + 1));
   RC(upload(E, (int32_t**)&c.jc, jc.data(), jc.size()));
+  {
+    std::vector<int32_t> jj(jc.size()), js(jc.size());
+    for (size_t q = 0; q < jc.size(); q++) {
+      jj[q] = net->lane_junction[jc[q]];
+      js[q] = net->lane_succ1[jc[q]];
+    }
+    c.n_conn = (int32_t)jc.size();
+    RC(upload(E, (int32_t**)&c.jc_junc, jj.data(), jj.size()));
+    RC(upload(E, (int32_t**)&c.jc_succ1, js.data(), js.size()));
+  }
   RC(upload(E, &c.sig, sig.data(), NJ));
   RC(upload(E, (VCold**)&c.cold, e->cold.data(), N));
   {
@@ -662,8 +731,8 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.cnt, NL));
   RC(dalloc(E, &c.cursor, NL));
   c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, N) / SCAN_TILE + 2);
-  RC(dalloc(E, &c.scan_status, c.scan_tiles_cap));
-  RC(dalloc(E, &c.scan_tiles, 1));
+  RC(dalloc(E, &c.scan_status, (size_t)SCAN_SITES * c.scan_tiles_cap));
+  RC(dalloc(E, &c.scan_tickets, SCAN_SITES));
   RC(dalloc(E, &c.stage, (size_t)NL + 1));
   RC(dalloc(E, &c.events, NL));
   RC(dalloc(E, &c.cl_idx, NL));
@@ -737,6 +806,7 @@ void tsb_destroy(tsb_engine* e) {
   for (void* p : e->allocs) cudaFree(p);
   if (e->dyn_host) cudaFreeHost(e->dyn_host);
   if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->body) cudaStreamDestroy(e->body);
   delete e;
 }
 

@@ -51,6 +51,15 @@ __device__ __forceinline__ int32_t* start_buf(const Ctx& c, int sel) {
 }
 __device__ __forceinline__ bool gated_off(const int32_t* gate) { return gate && *gate == 0; }
 
+// Conditional graph nodes (engine.cu issue_step): a section of the step graph
+// runs only when its deciding kernel sets the handle.  The handles default to
+// 0 at every graph launch; in eager launches (profiling, host-continuation
+// mode) use_cond is 0 and the sections' kernels gate themselves instead.
+enum { COND_RESOLVE = 0, COND_INJECT = 1, COND_PATCH = 2, COND_FULL = 3, N_COND = 4 };
+__device__ __forceinline__ void set_cond(const Ctx& c, int k, bool v) {
+  if (c.use_cond && v) cudaGraphSetConditional(c.cond[k], 1u);
+}
+
 // A lane whose membership or order changed after the sweep; the next
 // snapshot rebuilds only these lanes (k_patch_*), unless too many changed.
 __device__ __forceinline__ void mark_dirty(const Ctx& c, int32_t L) {
@@ -160,7 +169,14 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
 // (same leader, same gap, same cap).  Every reused value is the same fp64
 // expression on the same operands, so results are bit-identical to the
 // per-call evaluation.
-__global__ void __launch_bounds__(256, 2) k_update(Ctx c) {
+// Block size / min resident blocks of k_update (register budget: 64K / (BT * MINB)).
+#ifndef UPD_BT
+#define UPD_BT 256
+#endif
+#ifndef UPD_MINB
+#define UPD_MINB 3
+#endif
+__global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   Dyn* dy = c.dyn;
   const int32_t n = dy->n_a;
   const VRec* A = c.lay[dy->cur];
@@ -215,13 +231,27 @@ __global__ void __launch_bounds__(256, 2) k_update(Ctx c) {
         go = !(draw >= p.eval_prob);
       }
       if (go) {
+        // ---- evaluate_change (mobil.py:45-98) for each side.  All IDM
+        // calls are pure, so the side-independent ones (current leader, old
+        // follower) are evaluated once, up front and branch-free, and each
+        // side's three calls are evaluated together: independent fp64
+        // chains the scheduler can overlap instead of one long chain.
         const View mev{true, me.s, v};
         const View cl = view_at(A, i > lo0 ? i - 1 : -1);
         const View cf = view_at(A, i + 1 < hi0 ? i + 1 : -1);
-        // side-independent terms, computed on first use
-        bool have_common = false;
-        double a_me = 0.0, a_of = 0.0, a_of_new = 0.0;
         const double g_cur = gap_to(cl, me.s, Lv);
+        const double g_of_old = me.s - Lv - cf.s;
+        const double g_of_new = gap_to(cl, cf.s, Lv);
+        const bool of_ok = cf.ok && g_of_old > 0.0 && g_of_new > 0.0;
+        fr_me = idm_free(p, v, v0e_cur);
+        have_fr_me = true;
+        const double fr_cf = idm_free(p, cf.v, v0e_cur);
+        const double a_me_x = idm_safe(p, fr_me, v, dv_to(v, cl), g_cur);
+        const double a_of_x = idm_safe(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
+        const double a_of_new_x = idm_safe(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
+        const double a_me = (g_cur <= 0.0) ? -CUDART_INF : a_me_x;
+        const double a_of = of_ok ? a_of_x : 0.0;
+        const double a_of_new = of_ok ? a_of_new_x : 0.0;
         bool have = false;
         double best_inc = 0.0, best_s = 0.0;
         int32_t best_nb = -1;
@@ -237,51 +267,19 @@ __global__ void __launch_bounds__(256, 2) k_update(Ctx c) {
           const int32_t tl_i = m > 0 ? lo + m - 1 : -1;
           const View tl = view_at(A, tl_i);
           const View tf = view_at(A, lo + m < hi ? lo + m : -1);
-          // ---- evaluate_change (mobil.py:45-98)
           const double g_tl = gap_to(tl, s_t, Lv);
           const double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
-          if (g_tl <= 0.0 || g_tf <= 0.0) continue;
-          if (!have_common) {
-            have_common = true;
-            if (!(g_cur <= 0.0)) {
-              fr_me = idm_free(p, v, v0e_cur);
-              have_fr_me = true;
-              a_me = idm_with_free(p, fr_me, v, dv_to(v, cl), g_cur);
-            } else {
-              a_me = -CUDART_INF;
-            }
-            if (cf.ok) {
-              const double g_of_old = me.s - Lv - cf.s;
-              const double g_of_new = gap_to(cl, cf.s, Lv);
-              if (g_of_old > 0.0 && g_of_new > 0.0) {
-                const double fr_cf = idm_free(p, cf.v, v0e_cur);
-                a_of = idm_with_free(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
-                a_of_new = idm_with_free(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
-              }
-            }
-          }
+          const double g_nf_old = gap_to(tl, tf.s, Lv);
+          if (g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0)) continue;
           const double v0e_tgt = py_min(p.v0, LN.cap);
-          double fr_me_t;
-          if (have_fr_me && v0e_tgt == v0e_cur) {
-            fr_me_t = fr_me;
-          } else {
-            fr_me_t = idm_free(p, v, v0e_tgt);
-            if (v0e_tgt == v0e_cur) {
-              fr_me = fr_me_t;
-              have_fr_me = true;
-            }
-          }
-          const double a_me_new = idm_with_free(p, fr_me_t, v, dv_to(v, tl), g_tl);
-          double a_nf = 0.0, a_nf_new = 0.0;
-          if (tf.ok) {
-            const double g_nf_old = gap_to(tl, tf.s, Lv);
-            if (g_nf_old <= 0.0) continue;
-            const double fr_tf = idm_free(p, tf.v, v0e_tgt);
-            a_nf = idm_with_free(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
-            const View mt{true, s_t, v};
-            a_nf_new = idm_with_free(p, fr_tf, tf.v, dv_to(tf.v, mt), g_tf);
-            if (a_nf_new < -p.b_safe) continue;
-          }
+          const double fr_me_t = (v0e_tgt == v0e_cur) ? fr_me : idm_free(p, v, v0e_tgt);
+          const double fr_tf = idm_free(p, tf.v, v0e_tgt);
+          const double a_me_new = idm_safe(p, fr_me_t, v, dv_to(v, tl), g_tl);
+          const double a_nf_x = idm_safe(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
+          const double a_nf_new_x = idm_safe(p, fr_tf, tf.v, tf.v - v, g_tf);  // new leader: me at s_t
+          const double a_nf = tf.ok ? a_nf_x : 0.0;
+          const double a_nf_new = tf.ok ? a_nf_new_x : 0.0;
+          if (tf.ok && a_nf_new < -p.b_safe) continue;
           double inc;
           if (a_me == -CUDART_INF)
             inc = CUDART_INF;
@@ -302,7 +300,7 @@ __global__ void __launch_bounds__(256, 2) k_update(Ctx c) {
           changed = true;
           lane = best_nb;
           s = best_s;
-        } else if (have_common && cl.ok && g_cur >= EPS_GAP) {
+        } else if (cl.ok && g_cur >= EPS_GAP) {
           // world.py:406 will evaluate exactly a_me: same leader (i-1), gap
           // max(g_cur, 1e-6) == g_cur, same cap
           a_final = a_me;
@@ -484,21 +482,33 @@ __global__ void k_count_hostq(Ctx c) {
 // ------------------------------------------------------------------ scan
 
 // Exclusive scan of in[0, n) into out[0, n] (out[n] = total), single pass
-// with decoupled look-back.  status[] and *tiles must be zero on entry.
-// n is read from *n_dev when n_dev != nullptr.
+// with decoupled look-back.  n is read from *n_dev when n_dev != nullptr.
+// Every call site owns a status region and a 64-bit ticket counter that are
+// never reset: block b of invocation k draws ticket k * ntiles + b, and the
+// status words carry the invocation's epoch, so stale words from earlier
+// steps are ignored and the step graph needs no memset nodes.  All ntiles
+// blocks must be launched and draw a ticket (the gate is grid-uniform).
+static constexpr int SCAN_SITES = 4;
+enum { SCAN_LANES = 0, SCAN_INJ_LANES = 1, SCAN_INJ_RETRY = 2, SCAN_REGROUP = 3 };
 template <int BT, int IPT>
-__global__ void __launch_bounds__(BT) k_scan(Ctx c, const int32_t* in, int32_t* out, int out_sel, const int32_t* n_dev,
-                                             int32_t n_static, const int32_t* gate) {
+__global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in, int32_t* out, int out_sel,
+                                             const int32_t* n_dev, int32_t n_static, int32_t ntiles,
+                                             const int32_t* gate) {
   if (gated_off(gate)) return;
   if (out_sel != SEL_NONE) out = start_buf(c, out_sel);
-  unsigned long long* status = c.scan_status;
-  int32_t* tiles = c.scan_tiles;
+  unsigned long long* status = c.scan_status + (size_t)site * c.scan_tiles_cap;
   const int32_t n = n_dev ? *n_dev : n_static;
   __shared__ int32_t s_tile, s_prefix;
+  __shared__ unsigned s_epoch;
   __shared__ int32_t s_warp[BT / 32];
-  if (threadIdx.x == 0) s_tile = atomicAdd(tiles, 1);
+  if (threadIdx.x == 0) {
+    const unsigned long long t = atomicAdd(c.scan_tickets + site, 1ULL);
+    s_tile = (int32_t)(t % (unsigned long long)ntiles);
+    s_epoch = (unsigned)((t / (unsigned long long)ntiles) % 0x3fffffffULL) + 1u;
+  }
   __syncthreads();
   const int32_t tile = s_tile;
+  const unsigned long long ep = (unsigned long long)s_epoch << 34;
   const int64_t base = (int64_t)tile * BT * IPT;
   if (base > n) return;
   int32_t v[IPT];
@@ -533,26 +543,28 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, const int32_t* in, int32_t* 
   const int32_t total = s_warp[BT / 32 - 1];
   int32_t excl = warp_excl + x - local;
   if (threadIdx.x == 0) {
+    // status word: epoch (30 bits) | flag (2 bits) | value (32 bits);
+    // flag 1 = tile aggregate, 2 = inclusive prefix
     volatile unsigned long long* st = status;
     if (tile == 0) {
       __threadfence();
-      st[0] = (2ULL << 32) | (unsigned)total;
+      st[0] = ep | (2ULL << 32) | (unsigned)total;
       s_prefix = 0;
     } else {
-      st[tile] = (1ULL << 32) | (unsigned)total;
+      st[tile] = ep | (1ULL << 32) | (unsigned)total;
       __threadfence();
       int32_t acc = 0;
       int32_t t = tile - 1;
       for (;;) {
-        unsigned long long w = st[t];
-        unsigned flag = (unsigned)(w >> 32);
-        if (flag == 0) continue;
+        const unsigned long long w = st[t];
+        if ((w >> 34) != (ep >> 34)) continue;  // not yet published in this invocation
+        const unsigned flag = (unsigned)(w >> 32) & 3u;
         acc += (int32_t)(unsigned)(w & 0xffffffffULL);
         if (flag == 2) break;
         t--;
       }
       __threadfence();
-      st[tile] = (2ULL << 32) | (unsigned)(acc + total);
+      st[tile] = ep | (2ULL << 32) | (unsigned)(acc + total);
       s_prefix = acc;
     }
   }
@@ -573,6 +585,11 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, const int32_t* in, int32_t* 
 __global__ void k_scatter(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* n_extra, int start_sel,
                           const int32_t* gate) {
   if (gated_off(gate)) return;
+  if (src_sel == SEL_B && gtid() == 0) {
+    // vehicles bucketed into C this step (last CSR entry of the scan)
+    c.dyn->n_c = c.start[c.dyn->cur ^ 1][c.n_lanes];
+    if (c.dyn->n_hostq > 0 && !c.split) c.dyn->overflow |= 4;
+  }
   const VRec* src = rec_buf(c, src_sel);
   const int32_t* start = start_buf(c, start_sel);
   VRec* dst = c.D;
@@ -613,6 +630,12 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
   for (int32_t L = gtid() >> 5; L < c.n_lanes; L += warps) {
     const int32_t lo = start[L], hi = start[L + 1], n = hi - lo;
     if (n == 0) continue;
+    // the bucketing counters of this lane are consumed: leave them zero for
+    // the next use (replaces per-step memsets)
+    if (lane_id == 0) {
+      c.cnt[L] = 0;
+      c.cursor[L] = 0;
+    }
     // rank sort (keys unique: vix distinct)
     for (int32_t j = lane_id; j < n; j += 32) {
       const VRec r = D[lo + j];
@@ -1001,6 +1024,7 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
   __shared__ int32_t indeg[CL_CAP];
   __shared__ int32_t s_n, s_ne, s_over, s_changed, s_ncomp;
   const int32_t ne = dy->n_events;
+  if (threadIdx.x == 0) set_cond(c, COND_RESOLVE, ne > 0);
   // clear the previous step's closure marks
   for (int32_t q = threadIdx.x; q < dy->n_cl; q += blockDim.x) c.cl_idx[c.cl_lanes[q]] = 0;
   __syncthreads();
@@ -1278,15 +1302,24 @@ __global__ void k_signals(Ctx c) {
       }
     }
     c.sig[j] = st;
-    write_conn_flags(c, j, st);
+  }
+  if (gtid() == 0) {  // world.py:677-678 (nothing in this kernel reads the clock)
+    c.dyn->time += p.dt;
+    c.dyn->step_no += 1;
   }
 }
 
-__global__ void k_clock(Ctx c) {
-  Dyn* dy = c.dyn;
-  dy->time += c.p.dt;
-  dy->step_no += 1;
+// Connector flag bytes from the new junction states (thread per connector).
+__global__ void k_conn_flags(Ctx c) {
+  for (int32_t q = gtid(); q < c.n_conn; q += gstride()) {
+    const int32_t cn = c.jc[q], j = c.jc_junc[q];
+    uint8_t f = c.lflag[cn] & LF_OPEN;
+    if (c.lflag[c.jc_succ1[q]] & LF_OPEN) f |= LF_SUCC_OPEN;
+    f |= (uint8_t)(aspect_of(c, j, cn, c.sig[j]) << LF_ASPECT_SHIFT);
+    c.lflag[cn] = f;
+  }
 }
+
 
 // ------------------------------------------------------------------ injection (world.py:561-617)
 
@@ -1317,6 +1350,8 @@ __global__ void k_inject_due(Ctx c) {
     dy->pend_ptr = lo + nn;
     dy->n_due = nr + nn;
     dy->n_retry = 0;
+    dy->injected_now = 0;
+    set_cond(c, COND_INJECT, nr + nn > 0);
   }
 }
 
@@ -1346,6 +1381,8 @@ __global__ void k_inject_lanes(Ctx c) {
   for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) {
     const int32_t lo = c.inj_start[L], hi = c.inj_start[L + 1];
     if (hi == lo) continue;
+    c.inj_cnt[L] = 0;  // consumed: zero for the next injection (no memsets)
+    c.inj_cursor[L] = 0;
     // insertion sort of due positions
     for (int32_t a = lo + 1; a < hi; a++) {
       int32_t x = c.due_grp[a], b = a - 1;
@@ -1456,9 +1493,13 @@ __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
   const int nd = dy->n_dirty;
   if (!dy->need_regroup) return;
   if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
-    if (threadIdx.x == 0) dy->full_regroup = 1;
+    if (threadIdx.x == 0) {
+      dy->full_regroup = 1;
+      set_cond(c, COND_FULL, true);
+    }
     return;
   }
+  if (threadIdx.x == 0) set_cond(c, COND_PATCH, true);
   __shared__ int32_t sl[PATCH_MAX];
   __shared__ int32_t sd[PATCH_MAX];
   __shared__ int32_t warp_sum[32];
@@ -1576,28 +1617,34 @@ __global__ void k_patch_dirty(Ctx c) {
   }
 }
 
+// End of regroup: the new snapshot's size, or -- if nothing moved -- C (already
+// lane-sorted) becomes the snapshot by swapping the layout buffers.
 __global__ void k_patch_finish(Ctx c) {
   Dyn* dy = c.dyn;
-  if (dy->need_regroup && !dy->full_regroup) dy->n_a = dy->n_c + dy->n_inj;
   // clear dirty flags for the next step
   for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) c.dirty_flag[c.dirty_list[i]] = 0;
+  if (threadIdx.x == 0) {
+    if (!dy->need_regroup) {
+      dy->cur ^= 1;
+      dy->n_a = dy->n_c;
+    } else if (!dy->full_regroup) {
+      dy->n_a = dy->n_c + dy->n_inj;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ end of step
 
-// Choose the next snapshot: if nothing moved, C (already lane-sorted) is it.
-__global__ void k_commit_layout(Ctx c) {
-  Dyn* dy = c.dyn;
-  if (!dy->need_regroup) {
-    dy->cur ^= 1;
-    dy->n_a = dy->n_c;
-  }
-}
 
 // Per road, over the new snapshot: sum v and count (world.py:649-657).
 // Warp per road, fixed-order tree reduction (deterministic).
 __global__ void k_speeds(Ctx c) {
   Dyn* dy = c.dyn;
+  if (gtid() == 0) {  // end of step counters
+    dy->finished_total += dy->finished_now;
+    dy->reverts_total += dy->reverts_last;
+    dy->fin_log_n += dy->finished_now;
+  }
   const VRec* A = c.lay[dy->cur];
   const int32_t* S = c.start[dy->cur];
   const int32_t wi = (int32_t)(dy->time / c.p.speed_window);
@@ -1630,12 +1677,6 @@ __global__ void k_speeds(Ctx c) {
   }
 }
 
-__global__ void k_end_step(Ctx c) {
-  Dyn* dy = c.dyn;
-  dy->finished_total += dy->finished_now;
-  dy->reverts_total += dy->reverts_last;
-  dy->fin_log_n += dy->finished_now;
-}
 
 __global__ void k_begin_step(Ctx c) {
   Dyn* dy = c.dyn;
@@ -1653,11 +1694,6 @@ __global__ void k_begin_step(Ctx c) {
   dy->n_due = 0;
 }
 
-// After the scans: vehicle totals from the last CSR entry.
-__global__ void k_set_nc(Ctx c) {
-  c.dyn->n_c = c.start[c.dyn->cur ^ 1][c.n_lanes];
-  if (c.dyn->n_hostq > 0 && !c.split) c.dyn->overflow |= 4;
-}
 __global__ void k_set_na(Ctx c, const int32_t* gate) {
   if (gated_off(gate)) return;
   c.dyn->n_a = c.start[c.dyn->cur][c.n_lanes];
