@@ -118,6 +118,9 @@ struct Params {
   double politeness, threshold, b_safe, eval_prob;
   double L, speed_window, amber, s0_floor, mp_interval, mp_min_green;
   double sqrt_ab2;   // 2.0 * sqrt(a_max * b), evaluated as in idm.py:29
+  double inv_ab2;    // 1 / sqrt_ab2 when sqrt_ab2 is a power of two (then x / sqrt_ab2 == x * inv_ab2 exactly)
+  int32_t ab2_pow2;
+  uint64_t rng_h2;   // keyed-RNG fold state after (seed, STREAM_MOBIL): constant for the run
   int32_t controller;
   int32_t delta_int; // delta as an integer power if integral in [1, 64], else 0
   uint64_t seed;
@@ -132,6 +135,8 @@ struct Ctx {
   const LaneRec* lanes;
   const int32_t* succ;
   const int32_t* succ_dst_road;
+  const int4* succ_road4;  // per lane: roads of its first 4 successors (-5 = none)
+  const int4* succ_conn4;  // per lane: those successors (w = -2: more than 4; slots 3.. in the CSR)
   const int32_t* road_lane_off;
   const int32_t* road_lanes;
   const int32_t* junc_phase_off;
@@ -279,7 +284,8 @@ __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_
 // would take the division slow path for every leaderless vehicle.
 __device__ __forceinline__ double idm_with_free(const Params& p, double fr, double v, double dv, double gap) {
   const bool free_road = isinf(gap);
-  const double s_star = p.s0 + py_max(0.0, v * p.T + div_pos(v * dv, p.sqrt_ab2));
+  const double vdv = v * dv;
+  const double s_star = p.s0 + py_max(0.0, v * p.T + (p.ab2_pow2 ? vdv * p.inv_ab2 : div_pos(vdv, p.sqrt_ab2)));
   double g = free_road ? 1.0 : gap;
   asm("mov.b64 %0, %0;" : "+d"(g));
   const double q = div_pos(s_star, g);
@@ -304,6 +310,14 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
+}
+// The last two folds of keyed_uniform4(seed, 1, key, step) from the state
+// after the first two (a run constant, Params::rng_h2).
+__device__ __forceinline__ double keyed_uniform_tail(uint64_t h2, uint64_t key, uint64_t step) {
+  const uint64_t G = 0x9E3779B97F4A7C15ULL;
+  uint64_t h = mix64(h2 + G + key);
+  h = mix64(h + G + step);
+  return (double)(h >> 11) * 0x1p-53;
 }
 __device__ __forceinline__ double keyed_uniform4(uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
   const uint64_t G = 0x9E3779B97F4A7C15ULL;

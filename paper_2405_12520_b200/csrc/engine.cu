@@ -603,6 +603,19 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   P.mp_interval = p->mp_interval;
   P.mp_min_green = p->mp_min_green;
   P.sqrt_ab2 = 2.0 * std::sqrt(p->idm_a_max * p->idm_b);
+  {
+    int ex = 0;
+    const double m = std::frexp(P.sqrt_ab2, &ex);
+    P.ab2_pow2 = (m == 0.5 && std::isfinite(P.sqrt_ab2)) ? 1 : 0;
+    P.inv_ab2 = P.ab2_pow2 ? 1.0 / P.sqrt_ab2 : 0.0;
+    auto mix = [](uint64_t z) {
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+      return z ^ (z >> 31);
+    };
+    const uint64_t G = 0x9E3779B97F4A7C15ULL;
+    P.rng_h2 = mix(mix(0 + G + p->seed) + G + 1ULL);
+  }
   P.controller = p->controller;
   P.delta_int = (p->idm_delta == std::floor(p->idm_delta) && p->idm_delta >= 1 && p->idm_delta <= 64)
                     ? (int32_t)p->idm_delta
@@ -682,6 +695,22 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(upload(E, (LaneRec**)&c.lanes, e->lanes.data(), NL));
   RC(upload(E, (int32_t**)&c.succ, e->succ.data(), e->succ.size()));
   RC(upload(E, (int32_t**)&c.succ_dst_road, e->succ_dst_road.data(), e->succ_dst_road.size()));
+  {
+    std::vector<int4> r4(NL), k4(NL);
+    for (int32_t l = 0; l < NL; l++) {
+      int rr[4] = {-5, -5, -5, -5}, kk[4] = {-1, -1, -1, -1};
+      const LaneRec& L = e->lanes[l];
+      for (int q = 0; q < std::min<int>(L.nsucc, 4); q++) {
+        rr[q] = e->succ_dst_road[L.succ_off + q];
+        kk[q] = e->succ[L.succ_off + q];
+      }
+      if (L.nsucc > 4) kk[3] = -2, rr[3] = -5;  // slots 3.. are searched in the CSR
+      r4[l] = make_int4(rr[0], rr[1], rr[2], rr[3]);
+      k4[l] = make_int4(kk[0], kk[1], kk[2], kk[3]);
+    }
+    RC(upload(E, (int4**)&c.succ_road4, r4.data(), NL));
+    RC(upload(E, (int4**)&c.succ_conn4, k4.data(), NL));
+  }
   RC(upload(E, (int32_t**)&c.road_lane_off, net->road_lane_off, NR + 1));
   RC(upload(E, (int32_t**)&c.road_lanes, net->road_lanes, net->road_lane_off[NR]));
   RC(upload(E, (int32_t**)&c.junc_phase_off, net->junc_phase_off, NJ + 1));

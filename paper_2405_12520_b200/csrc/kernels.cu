@@ -80,6 +80,23 @@ __device__ __forceinline__ int32_t conn_from(const Ctx& c, const LaneRec& L, int
   return -1;
 }
 
+// Same, from the lane's 4-wide successor table (two independent 16 B loads
+// keyed by the lane id instead of a dependent walk of the CSR).
+__device__ __forceinline__ int32_t conn_from_id(const Ctx& c, int32_t lane, int32_t road) {
+  const int4 r = __ldg(c.succ_road4 + lane);
+  const int4 k = __ldg(c.succ_conn4 + lane);
+  if (r.x == road) return k.x;
+  if (r.y == road) return k.y;
+  if (r.z == road) return k.z;
+  if (r.w == road) return k.w;
+  if (k.w == -2) {  // more than 4 successors: the first 3 are in the table
+    const LaneRec L = c.lanes[lane];
+    for (int q = 3; q < L.nsucc; q++)
+      if (__ldg(c.succ_dst_road + L.succ_off + q) == road) return __ldg(c.succ + L.succ_off + q);
+  }
+  return -1;
+}
+
 __device__ __forceinline__ int lf_aspect(uint8_t f) { return (f >> LF_ASPECT_SHIFT) & 3; }
 // A connector a vehicle may enter: it and its successor lane are open
 // (world.py:282-283, 460-462).
@@ -209,7 +226,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     double best_a_new = 0.0, best_g_tl = 0.0;
     if (L0.kind == TSB_KIND_ROAD && (L0.left >= 0 || L0.right >= 0)) {
       const bool any = next_road < 0;
-      const bool mandatory = !any && conn_from(c, L0, next_road) < 0;
+      const bool mandatory = !any && conn_from_id(c, snap_lane, next_road) < 0;
       bool go = true;
       int32_t sides[2] = {L0.left, L0.right};
       int nsides = 2;
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         int32_t below = -1, above = -1;
         for (int32_t k = c.road_lane_off[L0.road]; k < c.road_lane_off[L0.road + 1]; k++) {
           int32_t f = c.road_lanes[k];
-          if (conn_from(c, c.lanes[f], next_road) < 0) continue;
+          if (conn_from_id(c, f, next_road) < 0) continue;
           if (f < lane && (below < 0 || f > below)) below = f;
           if (f > lane && (above < 0 || f < above)) above = f;
         }
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         nsides = 1;
       } else {
         const uint64_t key = c.ids_dense ? (uint64_t)me.vix : c.keys[me.vix];
-        double draw = keyed_uniform4(p.seed, 1ULL, key, step_no);
+        double draw = keyed_uniform_tail(p.rng_h2, key, step_no);  // rng.py:39-41 (seed, 1, id, step)
         go = !(draw >= p.eval_prob);
       }
       if (go) {
@@ -260,7 +277,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           if (nb < 0) continue;
           if (!(c.lflag[nb] & LF_OPEN)) continue;
           const LaneRec LN = c.lanes[nb];
-          if (!mandatory && !any && conn_from(c, LN, next_road) < 0) continue;
+          if (!mandatory && !any && conn_from_id(c, nb, next_road) < 0) continue;
           const double s_t = me.s * (LN.len / L0.len);
           const int32_t lo = S[nb], hi = S[nb + 1];
           const int32_t m = count_above(A, lo, hi, s_t);
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           lead_v = 0.0;
           found = true;
         } else {
-          const int32_t conn = conn_from(c, L1, next_road);
+          const int32_t conn = conn_from_id(c, lane, next_road);
           const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
           if (conn < 0 || !lf_passable(f)) {
             stop = true;
@@ -364,6 +381,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       if (!found) {
         const int32_t* rq = roads;
         LaneRec LC = L1;
+        int32_t cur = lane;
         double dist = remaining;
         gap = CUDART_INF;
         lead_v = 0.0;
@@ -371,7 +389,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           int32_t nxt;
           if (LC.kind == TSB_KIND_ROAD) {
             const int32_t nr = __ldg(rq + 1);
-            nxt = nr < 0 ? -1 : conn_from(c, LC, nr);
+            nxt = nr < 0 ? -1 : conn_from_id(c, cur, nr);
             if (nxt < 0 || !(c.lflag[nxt] & LF_OPEN)) break;
           } else {
             nxt = LC.succ1;
@@ -387,6 +405,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
             break;
           }
           LC = c.lanes[nxt];
+          cur = nxt;
           dist += LC.len;
         }
       }
@@ -423,7 +442,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           arrived = true;
           break;
         }
-        const int32_t conn = conn_from(c, LT, nr);
+        const int32_t conn = conn_from_id(c, nl, nr);
         const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
         if (conn >= 0 && !lf_passable(f)) {
           host = true;  // reroute needs the host router (world.py:460-469)
