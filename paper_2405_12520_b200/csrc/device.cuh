@@ -110,6 +110,7 @@ struct Dyn {
   int64_t reverts_total;
   int32_t n_cl;    // lanes in the revert closure (cleared at the next step)
   int32_t n_comp;  // closure components replayed in parallel
+  int32_t n_fix;   // lanes k_lanefix must sort / sweep this step
 };
 
 struct Params {
@@ -161,6 +162,11 @@ struct Ctx {
   VRec* D;
   int32_t* cnt;
   int32_t* cursor;
+  int32_t* ent;      // per lane: movers entering it this step
+  int32_t* ent_cur;
+  uint8_t* stay;     // per B record: still on its snapshot lane
+  int32_t* fix_flag;
+  int32_t* fix_list;
   unsigned long long* scan_status;   // SCAN_SITES regions of scan_tiles_cap words
   unsigned long long* scan_tickets;  // per scan site, never reset
   int32_t scan_tiles_cap;

@@ -193,7 +193,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   Ctx& c = e->c;
   Dyn* dy = c.dyn;
   const int VB = 256;
-  const int vgrid = grid_for(e->n_trips, VB, 148 * 8);
+  const int vgrid = grid_for(e->n_trips, VB, 1 << 30);  // one pass (no grid-stride tail)
   const int wgrid = grid_for((int64_t)e->n_lanes * 32, VB, 148 * 32);
   const int rgrid = grid_for((int64_t)e->n_roads * 32, VB, 148 * 16);
   const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
@@ -202,14 +202,15 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   const int32_t NL = e->n_lanes;
   if (phase != 2) {
     LAUNCH(KC_MISC, k_begin_step, 1, 1, c);
-    LAUNCH(KC_UPDATE, k_update, grid_for(e->n_trips, UPD_BT, 148 * 2048 / UPD_BT), UPD_BT, c);
+    cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
+    LAUNCH(KC_UPDATE, k_update, grid_for(e->n_trips, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
   // bucket the post-delta state by lane, sort each lane, tentative sweep
   scan(e, L, KC_SCAN, SCAN_LANES, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
-  LAUNCH(KC_SCATTER, k_scatter, vgrid, VB, c, SEL_B, &dy->n_a, nullptr, SEL_C, nullptr);
-  LAUNCH(KC_LANESORT_SWEEP, k_lanesort<true>, wgrid, VB, c, SEL_C, nullptr);
+  LAUNCH(KC_SCATTER, k_place, vgrid, VB, c);
+  LAUNCH(KC_LANESORT_SWEEP, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
   // exact revert resolution (only when some lane's sweep reverts)
   LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
   cond_begin(e, COND_RESOLVE);
@@ -243,6 +244,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_patch_dirty, 64, VB, c);
   cond_end(e);
   cond_begin(e, COND_FULL);
+  cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
   LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->full_regroup);
   scan(e, L, KC_REGROUP, SCAN_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
@@ -759,6 +761,11 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.D, N));
   RC(dalloc(E, &c.cnt, NL));
   RC(dalloc(E, &c.cursor, NL));
+  RC(dalloc(E, &c.ent, NL));
+  RC(dalloc(E, &c.ent_cur, NL));
+  RC(dalloc(E, &c.stay, N));
+  RC(dalloc(E, &c.fix_flag, NL));
+  RC(dalloc(E, &c.fix_list, NL));
   c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, N) / SCAN_TILE + 2);
   RC(dalloc(E, &c.scan_status, (size_t)SCAN_SITES * c.scan_tiles_cap));
   RC(dalloc(E, &c.scan_tickets, SCAN_SITES));

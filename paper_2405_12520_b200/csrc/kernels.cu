@@ -172,6 +172,14 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
   return a - lo;
 }
 
+// Post-update lane counts for the C layout; a vehicle that left its snapshot
+// lane is also a "mover" (k_place_movers / k_lanefix).
+__device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t snap_lane, int32_t i) {
+  atomicAdd(&c.cnt[lane], 1);
+  if (lane != snap_lane) atomicAdd(&c.ent[lane], 1);
+  c.stay[i] = lane == snap_lane ? 1 : 0;
+}
+
 // ------------------------------------------------------------------ k_update
 
 // World._update_vehicle + World._apply_deltas for one vehicle (thread per
@@ -192,6 +200,12 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
 #endif
 #ifndef UPD_MINB
 #define UPD_MINB 3
+#endif
+// One thread per vehicle (grid = ceil(N / BT) blocks, scheduled dynamically)
+// instead of a grid-stride loop: the last partial wave of a grid-stride
+// launch left most of the machine idle.
+#ifndef UPD_GRID_CAP
+#define UPD_GRID_CAP (1 << 30)
 #endif
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   Dyn* dy = c.dyn;
@@ -466,6 +480,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     VRec out{ns, nv, me.vix, nptr, nl, i};
     if (arrived) {
       out.lane = -1;
+      c.stay[i] = 0;
       c.status[me.vix] = TSB_STATUS_FINISHED;
       c.finish[me.vix] = new_time;
       c.fin_state[me.vix] = me;
@@ -480,10 +495,10 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       c.hostq[k] = i;
       if (!c.split) {  // closures only occur in split mode; keep the state consistent
         out.lane = nl;
-        atomicAdd(&c.cnt[nl], 1);
+        count_bucket(c, nl, snap_lane, i);
       }
     } else {
-      atomicAdd(&c.cnt[nl], 1);
+      count_bucket(c, nl, snap_lane, i);
     }
     c.B[i] = out;
   }
@@ -492,9 +507,14 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
 // Fix-up after host continuation of rerouted vehicles: count their lanes.
 __global__ void k_count_hostq(Ctx c) {
   Dyn* dy = c.dyn;
+  const VRec* A = c.lay[dy->cur];
   for (int32_t k = gtid(); k < dy->n_hostq; k += gstride()) {
-    const VRec r = c.B[c.hostq[k]];
-    if (r.lane >= 0) atomicAdd(&c.cnt[r.lane], 1);
+    const int32_t i = c.hostq[k];
+    const VRec r = c.B[i];
+    if (r.lane >= 0)
+      count_bucket(c, r.lane, A[i].lane, i);
+    else
+      c.stay[i] = 0;  // arrived during the host continuation
   }
 }
 
@@ -729,6 +749,158 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
           }
       }
     }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ lane assembly
+
+// Post-update lane assembly, the main path of the bucketing (replaces a full
+// scatter + per-lane sort).  B is in snapshot order, so the vehicles that
+// stayed on their lane ("stayers", nearly all) keep their relative order:
+// k_place writes each stayer straight to its C position (its snapshot rank
+// minus the lane's leavers ahead of it) and each mover to the tail of its new
+// lane's segment, and flags the lanes whose assembly is not final: a mover
+// entered, two stayers swapped order, or the sweep would touch a vehicle
+// (world.py:531 trigger).  k_lanefix then sorts (s desc, id asc) and sweeps
+// only the flagged lanes, on chip.
+__device__ __forceinline__ void flag_lane(const Ctx& c, int32_t L) {
+  if (atomicExch(&c.fix_flag[L], 1) == 0) c.fix_list[atomicAdd(&c.dyn->n_fix, 1)] = L;
+}
+
+__global__ void k_place(Ctx c) {
+  Dyn* dy = c.dyn;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const int32_t* SA = c.start[dy->cur];
+  const Params& p = c.p;
+  if (gtid() == 0) {
+    // vehicles bucketed into C this step (last CSR entry of the scan)
+    dy->n_c = CS[c.n_lanes];
+    if (dy->n_hostq > 0 && !c.split) dy->overflow |= 4;
+  }
+  const int32_t n = dy->n_a;
+  for (int32_t j = gtid(); j < n; j += gstride()) {
+    const VRec r = c.B[j];
+    const int32_t L = r.lane;
+    if (L < 0) continue;  // arrived
+    if (!c.stay[j]) {
+      const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + atomicAdd(&c.ent_cur[L], 1);
+      C[pos] = r;
+      flag_lane(c, L);
+      continue;
+    }
+    // rank among the lane's stayers: snapshot rank minus the leavers ahead
+    const int32_t a0 = SA[L];
+    int32_t lv = 0, k = -1;  // leavers ahead of j; previous stayer
+    for (int32_t q = j - 1; q >= a0; q--) {
+      if (c.stay[q]) {
+        if (k < 0) k = q;
+      } else {
+        lv++;
+      }
+    }
+    C[CS[L] + (j - a0) - lv] = r;
+    if (k >= 0) {
+      const VRec pr = c.B[k];
+      if (!ahead_of(pr.s, pr.vix, r.s, r.vix) || r.s > ((pr.s - p.L) - p.s0_floor) + 1e-12) flag_lane(c, L);
+    }
+  }
+}
+
+static constexpr int LX_CAP = 64;   // lane members staged in shared memory
+static constexpr int LX_WARPS = 8;
+__global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
+  __shared__ VRec s_in[LX_WARPS][LX_CAP];
+  __shared__ VRec s_out[LX_WARPS][LX_CAP];
+  Dyn* dy = c.dyn;
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const Params& p = c.p;
+  const int32_t nfix = dy->n_fix;
+  for (int32_t f = gtid() >> 5; f < nfix; f += warps) {
+    const int32_t L = c.fix_list[f];
+    const int32_t lo = CS[L], n = CS[L + 1] - lo;
+    if (lid == 0) {
+      c.fix_flag[L] = 0;
+      c.ent[L] = 0;  // consumed: zero for the next step (no memsets)
+      c.ent_cur[L] = 0;
+    }
+    const bool on_chip = n <= LX_CAP;
+    VRec* in = on_chip ? s_in[w] : c.D + lo;  // oversized lanes stage in D
+    VRec* out = on_chip ? s_out[w] : C + lo;
+    for (int32_t q = lid; q < n; q += 32) in[q] = C[lo + q];
+    __syncwarp();
+    // rank sort (keys unique: vix distinct)
+    for (int a = lid; a < n; a += 32) {
+      const double sa = in[a].s;
+      const int32_t va = in[a].vix;
+      int rank = 0;
+      for (int b2 = 0; b2 < n; b2++) rank += ahead_of(in[b2].s, in[b2].vix, sa, va) ? 1 : 0;
+      out[rank] = in[a];
+    }
+    __syncwarp();
+    // tentative sweep: parallel trigger test, then lane 0 from the first trigger
+    int32_t first = n;
+    for (int32_t j = lid; j < n; j += 32) {
+      if (j == 0) continue;
+      const double limit = (out[j - 1].s - p.L) - p.s0_floor;
+      if (out[j].s > limit + 1e-12) first = min(first, j);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if (first < n && lid == 0) {
+      VRec prev = out[first - 1];
+      bool prev_entered = prev.lane != A[prev.src].lane;
+      double prev_rear = prev.s - p.L;
+      bool event = false;
+      int32_t q = first;
+      for (; q < n; q++) {
+        VRec r = out[q];
+        const double limit = prev_rear - p.s0_floor;
+        const VRec sn = A[r.src];
+        const bool entered = r.lane != sn.lane;
+        if (r.s > limit + 1e-12) {
+          const double floor_s = entered ? 0.0 : sn.s;
+          if (limit >= floor_s) {
+            r.v = py_max(0.0, py_min(r.v, r.v - (r.s - limit) / p.dt));
+            r.s = limit;
+          } else if (entered || prev_entered) {  // a revert: resolved by k_resolve_*
+            event = true;
+            break;
+          } else {
+            r.v = 0.0;
+            r.s = floor_s;
+          }
+          out[q].s = r.s;
+          out[q].v = r.v;
+        }
+        prev_entered = entered;
+        prev_rear = r.s - p.L;
+      }
+      if (event) {
+        // leave the lane unswept (post-delta values) for the replay
+        for (int32_t u = first; u < q; u++) {
+          const VRec o = c.B[out[u].src];
+          out[u].s = o.s;
+          out[u].v = o.v;
+        }
+        c.events[atomicAdd(&dy->n_events, 1)] = L;
+      } else {
+        // a hold can break the (s desc) order; the next snapshot must be re-sorted
+        for (int32_t u = first - 1; u + 1 < n; u++)
+          if (!ahead_of(out[u].s, out[u].vix, out[u + 1].s, out[u + 1].vix)) {
+            mark_dirty(c, L);
+            break;
+          }
+      }
+    }
+    __syncwarp();
+    if (on_chip)
+      for (int a = lid; a < n; a += 32) C[lo + a] = out[a];
     __syncwarp();
   }
 }
@@ -1709,6 +1881,7 @@ __global__ void k_begin_step(Ctx c) {
   dy->need_regroup = 0;
   dy->n_inj = 0;
   dy->n_hostq = 0;
+  dy->n_fix = 0;
   dy->reverts_last = 0;
   dy->n_due = 0;
 }
