@@ -111,6 +111,9 @@ struct Dyn {
   int32_t n_cl;    // lanes in the revert closure (cleared at the next step)
   int32_t n_comp;  // closure components replayed in parallel
   int32_t n_fix;   // lanes k_lanefix must sort / sweep this step
+  int32_t speeds_pending;  // the snapshot's road aggregate is not yet accumulated
+  int32_t acc_now;         // this step's k_speeds branch accumulates it
+  double acc_time;         // the time of that snapshot
 };
 
 struct Params {
@@ -139,6 +142,7 @@ struct Ctx {
   const int4* succ_road4;  // per lane: roads of its first 4 successors (-5 = none)
   const int4* succ_conn4;  // per lane: those successors (w = -2: more than 4; slots 3.. in the CSR)
   const int32_t* road_lane_off;
+  const int2* road_span;  // per road: first and last lane id (consecutive ids)
   const int32_t* road_lanes;
   const int32_t* junc_phase_off;
   const double* phase_dur;

@@ -86,6 +86,8 @@ struct tsb_engine {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cur = nullptr;   // launch stream (see LAUNCH)
   cudaStream_t body = nullptr;  // captures conditional-section bodies
+  cudaStream_t side = nullptr;  // parallel branch (road aggregate)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraph_t body_graph = nullptr;
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
@@ -195,13 +197,19 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   const int VB = 256;
   const int vgrid = grid_for(e->n_trips, VB, 1 << 30);  // one pass (no grid-stride tail)
   const int wgrid = grid_for((int64_t)e->n_lanes * 32, VB, 148 * 32);
-  const int rgrid = grid_for((int64_t)e->n_roads * 32, VB, 148 * 16);
   const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
   const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
   const int cgrid = grid_for(std::max(c.n_conn, 1), VB, 148 * 8);
   const int32_t NL = e->n_lanes;
   if (phase != 2) {
     LAUNCH(KC_MISC, k_begin_step, 1, 1, c);
+    // previous step's road aggregate on a parallel branch (joined before the regroup)
+    cudaEventRecord(e->ev_fork, e->cur);
+    cudaStreamWaitEvent(e->side, e->ev_fork, 0);
+    L.pre(KC_SPEEDS);
+    k_speeds<<<grid_for((int64_t)std::max(e->n_roads, 1) * 32, VB, 1 << 30), VB, 0, e->side>>>(c, 0);
+    L.post();
+    cudaEventRecord(e->ev_join, e->side);
     cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
     LAUNCH(KC_UPDATE, k_update, grid_for(e->n_trips, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
   }
@@ -237,6 +245,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   cond_end(e);
   // next snapshot: nothing if no lane changed membership/order; else rebuild
   // only the dirty lanes and shift the rest; full regroup if too many changed
+  cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
   LAUNCH(KC_REGROUP, k_patch_prepare, 1, 1024, c);
   cond_begin(e, COND_PATCH);
   LAUNCH(KC_REGROUP, k_patch_starts, tgrid, VB, c);
@@ -252,7 +261,15 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
   cond_end(e);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
-  LAUNCH(KC_SPEEDS, k_speeds, rgrid, VB, c);
+}
+
+// Accumulates the current snapshot's road aggregate if the next step has not
+// done it yet (k_speeds); called before the aggregate is read.
+static int flush_speeds(tsb_engine* e) {
+  k_speeds<<<grid_for((int64_t)std::max(e->n_roads, 1) * 32, 256, 1 << 30), 256, 0, e->stream>>>(e->c, 1);
+  k_speeds_done<<<1, 1, 0, e->stream>>>(e->c);
+  CK(cudaGetLastError());
+  return TSB_OK;
 }
 
 // ----------------------------------------------------------------- host side pieces
@@ -575,6 +592,9 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->body, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
   e->cur = e->stream;
   const int32_t NL = e->n_lanes = net->n_lanes;
   const int32_t NR = e->n_roads = net->n_roads;
@@ -714,6 +734,18 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
     RC(upload(E, (int4**)&c.succ_conn4, k4.data(), NL));
   }
   RC(upload(E, (int32_t**)&c.road_lane_off, net->road_lane_off, NR + 1));
+  {
+    std::vector<int2> span(NR);
+    for (int32_t r = 0; r < NR; r++) {
+      const int32_t a = net->road_lane_off[r], b = net->road_lane_off[r + 1];
+      if (b <= a) return fail(TSB_EINVAL, "road %d has no lanes", r);
+      for (int32_t q = a + 1; q < b; q++)
+        if (net->road_lanes[q] != net->road_lanes[q - 1] + 1)
+          return fail(TSB_EINVAL, "road %d: lane ids must be consecutive (network.py:422-442)", r);
+      span[r] = make_int2(net->road_lanes[a], net->road_lanes[b - 1]);
+    }
+    RC(upload(E, (int2**)&c.road_span, span.data(), NR));
+  }
   RC(upload(E, (int32_t**)&c.road_lanes, net->road_lanes, net->road_lane_off[NR]));
   RC(upload(E, (int32_t**)&c.junc_phase_off, net->junc_phase_off, NJ + 1));
   RC(upload(E, (double**)&c.phase_dur, net->phase_dur, net->junc_phase_off[NJ]));
@@ -843,6 +875,9 @@ void tsb_destroy(tsb_engine* e) {
   if (e->dyn_host) cudaFreeHost(e->dyn_host);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->body) cudaStreamDestroy(e->body);
+  if (e->side) cudaStreamDestroy(e->side);
+  if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+  if (e->ev_join) cudaEventDestroy(e->ev_join);
   delete e;
 }
 
@@ -939,6 +974,7 @@ int tsb_finished(tsb_engine* e, int64_t since, int64_t cap, int32_t* vix, double
 }
 
 int tsb_road_acc(tsb_engine* e, int32_t n_windows, double* sum, int64_t* count) {
+  RC(flush_speeds(e));
   RC(sync_dyn(e));
   const int32_t W = e->c.n_win;
   std::vector<double> s((size_t)e->n_roads * W);

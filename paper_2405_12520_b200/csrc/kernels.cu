@@ -1821,6 +1821,11 @@ __global__ void k_patch_finish(Ctx c) {
     } else if (!dy->full_regroup) {
       dy->n_a = dy->n_c + dy->n_inj;
     }
+    // end of step counters
+    dy->finished_total += dy->finished_now;
+    dy->reverts_total += dy->reverts_last;
+    dy->fin_log_n += dy->finished_now;
+    dy->speeds_pending = 1;  // accumulated by the next k_update or a flush
   }
 }
 
@@ -1829,16 +1834,20 @@ __global__ void k_patch_finish(Ctx c) {
 
 // Per road, over the new snapshot: sum v and count (world.py:649-657).
 // Warp per road, fixed-order tree reduction (deterministic).
-__global__ void k_speeds(Ctx c) {
+// Road aggregate (world.py:649-657) of a step's final snapshot A: per road,
+// sum of v and count over its lanes.  Road lanes are consecutive ids
+// (network.py:422-442), so a road's vehicles are the contiguous range
+// [S[first lane], S[last lane + 1]) of A: warp per road, fixed-order tree
+// reduction (deterministic).  In the step graph this runs at the start of the
+// NEXT step on a parallel branch (A is only read until that step's regroup,
+// which joins it), hiding it behind the update; mode 1 is the flush a query
+// issues between steps.  Both use the same order.
+__global__ void k_speeds(Ctx c, int flush) {
   Dyn* dy = c.dyn;
-  if (gtid() == 0) {  // end of step counters
-    dy->finished_total += dy->finished_now;
-    dy->reverts_total += dy->reverts_last;
-    dy->fin_log_n += dy->finished_now;
-  }
+  if (!(flush ? dy->speeds_pending : dy->acc_now)) return;
   const VRec* A = c.lay[dy->cur];
   const int32_t* S = c.start[dy->cur];
-  const int32_t wi = (int32_t)(dy->time / c.p.speed_window);
+  const int32_t wi = (int32_t)((flush ? dy->time : dy->acc_time) / c.p.speed_window);
   if (wi >= c.n_win) {
     if (gtid() == 0) dy->overflow |= 2;
     return;
@@ -1846,27 +1855,22 @@ __global__ void k_speeds(Ctx c) {
   const int lane_id = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int32_t r = gtid() >> 5; r < c.n_roads; r += warps) {
+    const int2 span = c.road_span[r];
+    const int32_t j0 = S[span.x], j1 = S[span.y + 1];
+    if (j1 == j0) continue;
     double sum = 0.0;
-    int32_t cnt = 0;
-    for (int32_t q = c.road_lane_off[r]; q < c.road_lane_off[r + 1]; q++) {
-      const int32_t L = c.road_lanes[q];
-      for (int32_t j = S[L] + lane_id; j < S[L + 1]; j += 32) {
-        sum += A[j].v;
-        cnt += 1;
-      }
-    }
+    for (int32_t j = j0 + lane_id; j < j1; j += 32) sum += A[j].v;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    }
-    if (lane_id == 0 && cnt > 0) {
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane_id == 0) {
       const size_t cell = (size_t)r * c.n_win + wi;
       c.acc_sum[cell] += sum;
-      c.acc_cnt[cell] += cnt;
+      c.acc_cnt[cell] += j1 - j0;
     }
   }
 }
+
+__global__ void k_speeds_done(Ctx c) { c.dyn->speeds_pending = 0; }
 
 
 __global__ void k_begin_step(Ctx c) {
@@ -1882,6 +1886,9 @@ __global__ void k_begin_step(Ctx c) {
   dy->n_inj = 0;
   dy->n_hostq = 0;
   dy->n_fix = 0;
+  dy->acc_now = dy->speeds_pending;
+  dy->acc_time = dy->time;
+  dy->speeds_pending = 0;
   dy->reverts_last = 0;
   dy->n_due = 0;
 }
