@@ -780,27 +780,39 @@ __global__ void k_place(Ctx c) {
     if (dy->n_hostq > 0 && !c.split) dy->overflow |= 4;
   }
   const int32_t n = dy->n_a;
-  for (int32_t j = gtid(); j < n; j += gstride()) {
-    const VRec r = c.B[j];
+  const int lid = threadIdx.x & 31;
+  // one pass, whole warps (the ballots below need all 32 lanes)
+  for (int32_t base = (gtid() >> 5) << 5; base < n; base += gstride()) {
+    const int32_t j = base + lid;
+    const bool valid = j < n;
+    const VRec r = valid ? c.B[j] : VRec{0.0, 0.0, 0, 0, -1, 0};
+    const bool st = valid && c.stay[j];
+    const unsigned stay_bits = __ballot_sync(0xffffffffu, st);
     const int32_t L = r.lane;
-    if (L < 0) continue;  // arrived
-    if (!c.stay[j]) {
+    if (!valid || L < 0) continue;  // arrived (no ballots follow)
+    if (!st) {
       const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + atomicAdd(&c.ent_cur[L], 1);
       C[pos] = r;
       flag_lane(c, L);
       continue;
     }
-    // rank among the lane's stayers: snapshot rank minus the leavers ahead
+    // rank among the lane's stayers: stayers ahead of j in its snapshot
+    // segment [a0, j) -- inside this warp from the ballot, before it by a
+    // short loop (only for the warp's first segment)
     const int32_t a0 = SA[L];
-    int32_t lv = 0, k = -1;  // leavers ahead of j; previous stayer
-    for (int32_t q = j - 1; q >= a0; q--) {
+    const int lo_lane = a0 > base ? a0 - base : 0;
+    const unsigned below = (1u << lid) - 1u, from = ~((1u << lo_lane) - 1u);
+    int32_t rank = __popc(stay_bits & below & from);
+    int32_t k = -1;  // previous stayer
+    const unsigned prev_bits = stay_bits & below & from;
+    if (prev_bits) k = base + 31 - __clz(prev_bits);
+    for (int32_t q = base - 1; q >= a0; q--) {
       if (c.stay[q]) {
+        rank++;
         if (k < 0) k = q;
-      } else {
-        lv++;
       }
     }
-    C[CS[L] + (j - a0) - lv] = r;
+    C[CS[L] + rank] = r;
     if (k >= 0) {
       const VRec pr = c.B[k];
       if (!ahead_of(pr.s, pr.vix, r.s, r.vix) || r.s > ((pr.s - p.L) - p.s0_floor) + 1e-12) flag_lane(c, L);
