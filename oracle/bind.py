@@ -52,6 +52,7 @@ def lib():
         L.orc_idm_accel.restype = C.c_double
         L.orc_keyed_uniform4.argtypes = [C.c_uint64] * 4
         L.orc_keyed_uniform4.restype = C.c_double
+        L.orc_set_threads.argtypes = [vp, C.c_int32]
         L.orc_pow_cr.argtypes = [C.c_double, C.c_int32]
         L.orc_pow_cr.restype = C.c_double
         _LIB = L
@@ -77,6 +78,9 @@ class OracleWorld:
         self._h = h
         self._fin_seen = 0
         self.finished: list[tuple[int, float, float]] = []
+
+    def set_threads(self, n: int):
+        lib().orc_set_threads(self._h, n)
 
     def close(self):
         if self._h:

@@ -21,6 +21,7 @@
  * produced by tests/golden/make_golden.py from the reference itself).
  */
 #include <float.h>
+#include <pthread.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -110,6 +111,7 @@ struct orc {
   double* fin_t;
   int64_t fin_cap;
   int64_t dropped, vehicle_updates, step_no, injected_now, finished_now, reverts_last, reverts_total;
+  int threads; /* update-phase threads (orc_set_threads) */
   double time;
   /* speed accumulators [road][window] */
   int32_t nwin;
@@ -950,13 +952,47 @@ static void compact_driving(orc* o) {
   o->drv.n = m;
 }
 
+typedef struct {
+  orc* o;
+  const int32_t* order;
+  int32_t lo, hi;
+} upd_job;
+
+static void* upd_worker(void* arg) {
+  upd_job* j = (upd_job*)arg;
+  for (int32_t k = j->lo; k < j->hi; k++) update_vehicle(j->o, j->order[k]);
+  return NULL;
+}
+
+static void update_parallel(orc* o, const int32_t* order, int32_t n) {
+  int t = o->threads;
+  if (t <= 1 || n < 256) {
+    for (int32_t k = 0; k < n; k++) update_vehicle(o, order[k]);
+    return;
+  }
+  if (t > 256) t = 256;
+  pthread_t th[256];
+  upd_job jobs[256];
+  for (int q = 0; q < t; q++) {
+    jobs[q].o = o;
+    jobs[q].order = order;
+    jobs[q].lo = (int32_t)((int64_t)n * q / t);
+    jobs[q].hi = (int32_t)((int64_t)n * (q + 1) / t);
+    pthread_create(&th[q], NULL, upd_worker, &jobs[q]);
+  }
+  for (int q = 0; q < t; q++) pthread_join(th[q], NULL);
+}
+
 /* world.py:659-689 */
 static void step_once(orc* o) {
   int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(o->n_driving + 1));
   int32_t n = sorted_driving(o, order);
   build_index(o, order, n);
   o->vehicle_updates += n;
-  for (int32_t k = 0; k < n; k++) update_vehicle(o, order[k]);
+  /* The update phase reads only the snapshot and writes each vehicle's own
+   * deltas (world.py:664-669): the reference's thread-pool
+   * chunking restated with pthreads.  Results do not depend on the thread count. */
+  update_parallel(o, order, n);
   o->finished_now = apply_deltas(o, order, n);
   compact_driving(o);
   collision_sweep(o);
@@ -986,6 +1022,7 @@ static int cmp_pending(const void* a, const void* b) {
 
 int orc_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, orc** out) {
   orc* o = (orc*)calloc(1, sizeof(orc));
+  o->threads = 1;
   o->p = *p;
   int32_t nl = o->nl = net->n_lanes;
   o->nr = net->n_roads;
@@ -1192,6 +1229,12 @@ int orc_route_cost(orc* o, int32_t origin, int32_t dest, double* cost, int32_t* 
   free(rs);
   *n_roads = n < 0 ? 0 : n;
   *cost = n < 0 ? -1.0 : dist_to(o, dest)[origin];
+  return OK;
+}
+
+/* Threads for the update phase (EngineConfig.threads, params.py:48-83). */
+int orc_set_threads(orc* o, int32_t n) {
+  o->threads = n < 1 ? 1 : n;
   return OK;
 }
 
