@@ -114,6 +114,27 @@ int tsb_create(const tsb_network* net, const tsb_trips* trips, const tsb_params*
 void tsb_destroy(tsb_engine* e); /* World.close (world.py:827-830) */
 const char* tsb_last_error(void);
 
+/* Sharded (multi-GPU) engine: lanes partitioned into spatial
+ * bands, each rank simulating its own lanes plus a halo of ghost lanes
+ * (paper_2405_12520_b200/shard.py computes the plan).  No reference
+ * counterpart: the reference is single-process (world.py:664-669 threads). */
+typedef struct tsb_shard {
+  int32_t rank, nranks;        /* 1 <= nranks <= 8 */
+  const uint8_t* zone;         /* per lane: 1 own, 2 halo (ghost), | 4 computed exactly; 0 outside */
+  const int32_t* export_off;   /* [nranks+1] CSR over export_lanes, by destination rank */
+  const int32_t* export_lanes; /* own lanes in each peer's halo, ascending */
+  const int32_t* import_off;   /* [nranks+1] CSR over import_lanes, by source rank */
+  const int32_t* import_lanes; /* each peer's lanes in my halo, ascending */
+} tsb_shard;
+int tsb_create_sharded(const tsb_network* net, const tsb_trips* trips, const tsb_params* p, int32_t device,
+                       const tsb_shard* shard, tsb_engine** out);
+/* After a step: pack the boundary lanes for every peer into `send` (device
+ * memory of `cap` bytes); bytes[q] = size of the message to rank q. */
+int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes);
+/* Before the next step: ghosts from `recv` (device memory, the peers'
+ * messages concatenated in rank order, bytes[q] each). */
+int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes);
+
 /* World.step() x n (world.py:659-689); report of the last step (may be NULL). */
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last);
 /* Current counters without stepping. */

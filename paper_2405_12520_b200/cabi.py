@@ -62,6 +62,15 @@ class TsbReport(C.Structure):
                                  "resolve_sequential", "reverts_total")]
 
 
+class TsbShard(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32), ("nranks", C.c_int32),
+        ("zone", _p(C.c_uint8)),
+        ("export_off", _p(C.c_int32)), ("export_lanes", _p(C.c_int32)),
+        ("import_off", _p(C.c_int32)), ("import_lanes", _p(C.c_int32)),
+    ]
+
+
 _CT = {np.float64: C.c_double, np.int8: C.c_int8, np.uint8: C.c_uint8,
        np.int32: C.c_int32, np.uint64: C.c_uint64, np.int64: C.c_int64}
 
@@ -108,6 +117,23 @@ def pack_trips(t: FlatTrips) -> Packed:
               "dest_lane": np.int32, "departure": np.float64}
     keep = {k: _nonempty(getattr(t, k), tp) for k, tp in fields.items()}
     s = TsbTrips(n=len(t.ids), **{k: ptr(a, fields[k]) for k, a in keep.items()})
+    return Packed(s, keep)
+
+
+def pack_shard(plan) -> Packed:
+    """tsb_shard from a shard.ShardPlan."""
+    def csr(lists):
+        off = np.zeros(len(lists) + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(x) for x in lists])
+        flat = np.concatenate([np.asarray(x, dtype=np.int32) for x in lists]) if lists else np.zeros(0, np.int32)
+        return off, _nonempty(flat, np.int32)
+    eo, el = csr(plan.export_lanes)
+    io, il = csr(plan.import_lanes)
+    zone = _nonempty(plan.zone, np.uint8)
+    keep = dict(zone=zone, eo=eo, el=el, io=io, il=il)
+    s = TsbShard(rank=plan.rank, nranks=plan.nranks, zone=ptr(zone, np.uint8),
+                 export_off=ptr(eo, np.int32), export_lanes=ptr(el, np.int32),
+                 import_off=ptr(io, np.int32), import_lanes=ptr(il, np.int32))
     return Packed(s, keep)
 
 

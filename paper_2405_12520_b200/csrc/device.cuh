@@ -111,6 +111,8 @@ struct Dyn {
   int32_t n_cl;    // lanes in the revert closure (cleared at the next step)
   int32_t n_comp;  // closure components replayed in parallel
   int32_t n_fix;   // lanes k_lanefix must sort / sweep this step
+  int32_t n_g;     // sharded: ghost records appended to the snapshot at [n_a, n_a + n_g)
+  int32_t n_own;   // sharded: vehicles on own lanes in the snapshot
   int32_t speeds_pending;  // the snapshot's road aggregate is not yet accumulated
   int32_t acc_now;         // this step's k_speeds branch accumulates it
   double acc_time;         // the time of that snapshot
@@ -134,6 +136,7 @@ struct Params {
 struct Ctx {
   Params p;
   int32_t n_lanes, n_roads, n_junc, n_trips;
+  int32_t n_pend;  // trips in the pending list (all, or a shard's own)
   int32_t split;  // 1 when lane closures exist: host continuation of reroutes
   int32_t debug;  // test knobs: 1 = always sequential resolve, 2 = always full regroup
   const LaneRec* lanes;
@@ -174,6 +177,22 @@ struct Ctx {
   unsigned long long* scan_status;   // SCAN_SITES regions of scan_tiles_cap words
   unsigned long long* scan_tickets;  // per scan site, never reset
   int32_t scan_tiles_cap;
+  // sharded mode (shard.py): per-lane zone flags, ghost ranges, export/import lists
+  int32_t sharded;
+  const uint8_t* zone;  // ZF_OWN | ZF_HALO, ZF_EXACT
+  int2* ghost_seg;      // per halo lane: [start, end) of its ghosts in the snapshot buffer
+  int32_t n_exp, n_imp;
+  const int32_t* exp_lane;  // export entries (peer-major, ascending lanes)
+  const int32_t* exp_peer;
+  const int32_t* imp_lane;  // import entries (source-major, ascending lanes)
+  const int32_t* imp_peer;
+  int32_t* exp_cnt;
+  int32_t* exp_pos;  // exclusive scan of exp_cnt (n_exp + 1)
+  int32_t* imp_cnt;
+  int32_t* imp_pos;
+  int64_t peer_first_exp[9], peer_first_imp[9];  // entry index ranges per peer (nranks <= 8)
+  int32_t nranks, rank;
+  int32_t* comp_flags;  // per component: bit 0 has an own lane, bit 1 has an inexact lane
   // conditional sections of the step graph (kernels.cu set_cond)
   unsigned long long cond[4];
   int32_t use_cond;

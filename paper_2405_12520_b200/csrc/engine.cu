@@ -68,6 +68,8 @@ struct tsb_engine {
   std::vector<void*> allocs;
   // host copies (authoritative for control changes and host continuation)
   int32_t n_lanes = 0, n_roads = 0, n_junc = 0, n_trips = 0;
+  int32_t n_pend = 0;  // trips this engine injects (all, or the shard's own)
+  int64_t cap = 0;     // record capacity of the vehicle layouts (2N when sharded: own + ghosts)
   std::vector<LaneRec> lanes;
   std::vector<int32_t> succ, succ_dst_road;
   std::vector<double> phase_dur;
@@ -195,7 +197,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   Ctx& c = e->c;
   Dyn* dy = c.dyn;
   const int VB = 256;
-  const int vgrid = grid_for(e->n_trips, VB, 1 << 30);  // one pass (no grid-stride tail)
+  const int vgrid = grid_for(e->cap, VB, 1 << 30);  // one pass (no grid-stride tail)
   const int wgrid = grid_for((int64_t)e->n_lanes * 32, VB, 148 * 32);
   const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
   const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
@@ -211,7 +213,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     L.post();
     cudaEventRecord(e->ev_join, e->side);
     cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
-    LAUNCH(KC_UPDATE, k_update, grid_for(e->n_trips, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+    LAUNCH(KC_UPDATE, k_update, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
@@ -261,6 +263,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
   cond_end(e);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
+  if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
 }
 
 // Accumulates the current snapshot's road aggregate if the next step has not
@@ -583,8 +586,55 @@ extern "C" {
 
 const char* tsb_last_error(void) { return g_err.c_str(); }
 
-int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device, tsb_engine** out) {
+// Sharded mode: zone flags, export/import entry lists (static per run).
+static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
+  Ctx& c = e->c;
+  const int32_t NL = e->n_lanes;
+  c.sharded = 1;
+  c.rank = sh->rank;
+  c.nranks = sh->nranks;
+  RC(upload(e, (uint8_t**)&c.zone, sh->zone, NL));
+  RC(dalloc(e, &c.ghost_seg, NL));
+  std::vector<int32_t> el, ep, il, ip;
+  for (int q = 0; q < sh->nranks; q++) {
+    c.peer_first_exp[q] = (int64_t)el.size();
+    c.peer_first_imp[q] = (int64_t)il.size();
+    for (int32_t k = sh->export_off[q]; k < sh->export_off[q + 1]; k++) {
+      el.push_back(sh->export_lanes[k]);
+      ep.push_back(q);
+    }
+    for (int32_t k = sh->import_off[q]; k < sh->import_off[q + 1]; k++) {
+      if (!(sh->zone[sh->import_lanes[k]] & 2)) return fail(TSB_EINVAL, "import lane %d is not a halo lane", sh->import_lanes[k]);
+      il.push_back(sh->import_lanes[k]);
+      ip.push_back(q);
+    }
+  }
+  for (int q = sh->nranks; q < 9; q++) {
+    c.peer_first_exp[q] = (int64_t)el.size();
+    c.peer_first_imp[q] = (int64_t)il.size();
+  }
+  c.n_exp = (int32_t)el.size();
+  c.n_imp = (int32_t)il.size();
+  RC(upload(e, (int32_t**)&c.exp_lane, el.data(), el.size()));
+  RC(upload(e, (int32_t**)&c.exp_peer, ep.data(), ep.size()));
+  RC(upload(e, (int32_t**)&c.imp_lane, il.data(), il.size()));
+  RC(upload(e, (int32_t**)&c.imp_peer, ip.data(), ip.size()));
+  RC(dalloc(e, &c.exp_cnt, el.size() + 1));
+  RC(dalloc(e, &c.exp_pos, el.size() + 1));
+  RC(dalloc(e, &c.imp_cnt, il.size() + 1));
+  RC(dalloc(e, &c.imp_pos, il.size() + 1));
+  RC(dalloc(e, &c.comp_flags, 2048));
+  if ((int64_t)std::max(el.size(), il.size()) / SCAN_TILE + 2 > c.scan_tiles_cap)
+    return fail(TSB_ECAP, "too many exchange lanes for the scan scratch");
+  return TSB_OK;
+}
+
+static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device,
+                       const tsb_shard* sh, tsb_engine** out) {
   if (!net || !tr || !p || !out) return fail(TSB_EINVAL, "null argument");
+  if (sh && (sh->nranks < 1 || sh->nranks > 8 || sh->rank < 0 || sh->rank >= sh->nranks || !sh->zone))
+    return fail(TSB_EINVAL, "bad shard description (1 <= nranks <= 8)");
+  if (sh && p->controller != 0) return fail(TSB_EINVAL, "sharded mode supports fixed-time signals only");
   if (p->pow_mode != 0)
     return fail(TSB_EINVAL, "pow_mode %d unsupported on device (0 = correctly rounded powers)", p->pow_mode);
   auto e = std::make_unique<tsb_engine>();
@@ -600,6 +650,7 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   const int32_t NR = e->n_roads = net->n_roads;
   const int32_t NJ = e->n_junc = net->n_junctions;
   const int32_t N = e->n_trips = tr->n;
+  const int64_t CAP = e->cap = sh ? 2 * (int64_t)N : (int64_t)N;
   Ctx& c = e->c;
   c.n_lanes = NL;
   c.n_roads = NR;
@@ -703,11 +754,17 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
     e->dest[k] = tr->dest_lane[k];
     pend[k] = k;
   }
+  if (sh) {  // a rank injects the trips whose origin lane it owns
+    pend.erase(std::remove_if(pend.begin(), pend.end(),
+                              [&](int32_t k) { return !(sh->zone[tr->origin_lane[k]] & 1); }),
+               pend.end());
+  }
   std::stable_sort(pend.begin(), pend.end(), [&](int32_t a, int32_t b) {
     return tr->departure[a] < tr->departure[b];  // ties keep ascending id
   });
-  std::vector<double> pend_dep(N);
-  for (int32_t k = 0; k < N; k++) pend_dep[k] = tr->departure[pend[k]];
+  const int32_t NP = e->n_pend = c.n_pend = (int32_t)pend.size();
+  std::vector<double> pend_dep(NP);
+  for (int32_t k = 0; k < NP; k++) pend_dep[k] = tr->departure[pend[k]];
 
   e->router = std::make_unique<Router>(NL, net->lane_kind, net->lane_len, net->lane_cap, net->lane_open,
                                        net->succ_off, net->succ, net->pred_off, net->pred, net->lane_road);
@@ -775,8 +832,8 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
     for (int32_t l = 0; l < NL; l++) lf[l] = net->lane_open[l] ? LF_OPEN : 0;
     RC(upload(E, &c.lflag, lf.data(), NL));
   }
-  RC(upload(E, (int32_t**)&c.pend_vix, pend.data(), N));
-  RC(upload(E, (double**)&c.pend_dep, pend_dep.data(), N));
+  RC(upload(E, (int32_t**)&c.pend_vix, pend.data(), NP));
+  RC(upload(E, (double**)&c.pend_dep, pend_dep.data(), NP));
   RC(dalloc(E, &c.status, N));
   RC(dalloc(E, &c.routed, N));
   RC(dalloc(E, &c.finish, N));
@@ -786,19 +843,19 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
     if (N) CK(cudaMemcpy(c.finish, nanv.data(), sizeof(double) * N, cudaMemcpyHostToDevice));
   }
   for (int b = 0; b < 2; b++) {
-    RC(dalloc(E, &c.lay[b], N));
+    RC(dalloc(E, &c.lay[b], CAP));
     RC(dalloc(E, &c.start[b], (size_t)NL + 1));
   }
-  RC(dalloc(E, &c.B, N));
-  RC(dalloc(E, &c.D, N));
+  RC(dalloc(E, &c.B, CAP));
+  RC(dalloc(E, &c.D, CAP));
   RC(dalloc(E, &c.cnt, NL));
   RC(dalloc(E, &c.cursor, NL));
   RC(dalloc(E, &c.ent, NL));
   RC(dalloc(E, &c.ent_cur, NL));
-  RC(dalloc(E, &c.stay, N));
+  RC(dalloc(E, &c.stay, CAP));
   RC(dalloc(E, &c.fix_flag, NL));
   RC(dalloc(E, &c.fix_list, NL));
-  c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, N) / SCAN_TILE + 2);
+  c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, CAP) / SCAN_TILE + 2);
   RC(dalloc(E, &c.scan_status, (size_t)SCAN_SITES * c.scan_tiles_cap));
   RC(dalloc(E, &c.scan_tickets, SCAN_SITES));
   RC(dalloc(E, &c.stage, (size_t)NL + 1));
@@ -816,15 +873,15 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.patch_lanes, 4096));
   RC(dalloc(E, &c.patch_count, 4096));
   RC(dalloc(E, &c.patch_prefix, 4097));
-  RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)N + 16));
+  RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)CAP + 16));
   RC(dalloc(E, &c.rs_inwork, NL));
   RC(dalloc(E, &c.rs_touched, NL));
   RC(dalloc(E, &c.rs_event, NL));
   RC(dalloc(E, &c.rs_movedin, NL));
-  RC(dalloc(E, &c.rs_moved, N));
-  RC(dalloc(E, &c.rs_reverted, N));
-  RC(dalloc(E, &c.rs_members, N));
-  RC(dalloc(E, &c.rs_touched_list, (size_t)NL + N));
+  RC(dalloc(E, &c.rs_moved, CAP));
+  RC(dalloc(E, &c.rs_reverted, CAP));
+  RC(dalloc(E, &c.rs_members, CAP));
+  RC(dalloc(E, &c.rs_touched_list, (size_t)NL + CAP));
   RC(dalloc(E, &c.retry, N));
   RC(dalloc(E, &c.retry2, N));
   RC(dalloc(E, &c.due, N));
@@ -837,7 +894,8 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   RC(dalloc(E, &c.flag_scan, (size_t)N + 1));
   RC(dalloc(E, &c.lane_counts, NL));
   RC(dalloc(E, &c.fin_log, N));
-  RC(dalloc(E, &c.hostq, N));
+  RC(dalloc(E, &c.hostq, CAP));
+  if (sh) RC(setup_shard(E, sh));
   RC(dalloc(E, &c.dyn, 1));
   RC(dalloc(E, &c.scratch_d, 16));
   CK(cudaMallocHost((void**)&e->dyn_host, sizeof(Dyn)));
@@ -864,6 +922,64 @@ int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p,
   return TSB_OK;
 }
 
+int tsb_create(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device, tsb_engine** out) {
+  return create_impl(net, tr, p, device, nullptr, out);
+}
+
+int tsb_create_sharded(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device,
+                       const tsb_shard* sh, tsb_engine** out) {
+  if (!sh) return fail(TSB_EINVAL, "null shard description");
+  return create_impl(net, tr, p, device, sh, out);
+}
+
+int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes) {
+  if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
+  Ctx& c = e->c;
+  if (c.n_exp > 0) {
+    k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, e->stream>>>(c);
+    const int ntiles = c.n_exp / SCAN_TILE + 1;
+    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, e->stream>>>(c, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE,
+                                                                 nullptr, c.n_exp, ntiles, nullptr);
+  }
+  std::vector<int32_t> pos(c.n_exp + 1, 0);
+  if (c.n_exp > 0) CK(cudaMemcpyAsync(pos.data(), c.exp_pos, sizeof(int32_t) * (c.n_exp + 1), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  int64_t total = 0;
+  for (int q = 0; q < c.nranks; q++) {
+    const int64_t e0 = c.peer_first_exp[q], e1 = c.peer_first_exp[q + 1];
+    bytes[q] = e1 > e0 ? ((4 * (e1 - e0) + 31) & ~(int64_t)31) + 32 * (int64_t)(pos[e1] - pos[e0]) : 0;
+    total += bytes[q];
+  }
+  if (total > cap) return fail(TSB_ECAP, "send buffer too small (%lld > %lld bytes)", (long long)total, (long long)cap);
+  if (c.n_exp > 0) k_exp_pack<<<grid_for((int64_t)c.n_exp * 32, 256, 1 << 20), 256, 0, e->stream>>>(c, (uint8_t*)send);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(e->stream));
+  return TSB_OK;
+}
+
+int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes) {
+  if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
+  Ctx& c = e->c;
+  SrcBase sb{};
+  int64_t acc = 0;
+  for (int q = 0; q < c.nranks; q++) {
+    sb.b[q] = acc;
+    acc += bytes[q];
+  }
+  RC(sync_dyn(e));
+  if ((int64_t)e->dyn_host->n_a + (int64_t)e->n_trips > e->cap) return fail(TSB_ECAP, "ghost capacity");
+  if (c.n_imp > 0) {
+    k_imp_count<<<grid_for(c.n_imp, 256, 1 << 20), 256, 0, e->stream>>>(c, (const uint8_t*)recv, sb);
+    const int ntiles = c.n_imp / SCAN_TILE + 1;
+    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, e->stream>>>(c, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE,
+                                                                 nullptr, c.n_imp, ntiles, nullptr);
+    k_imp_copy<<<grid_for((int64_t)c.n_imp * 32, 256, 1 << 20), 256, 0, e->stream>>>(c, (const uint8_t*)recv, sb);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(e->stream));
+  return TSB_OK;
+}
+
 void tsb_destroy(tsb_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
@@ -885,8 +1001,8 @@ static void fill_report(const tsb_engine* e, tsb_report* r) {
   const Dyn& d = *e->dyn_host;
   r->time = d.time;
   r->step_no = d.step_no;
-  r->driving = d.n_a;
-  r->waiting = (int64_t)(e->n_trips - d.pend_ptr) + d.n_retry;
+  r->driving = e->c.sharded ? d.n_own : d.n_a;
+  r->waiting = (int64_t)(e->n_pend - d.pend_ptr) + d.n_retry;
   r->finished = d.finished_total;
   r->dropped = d.dropped;
   r->injected_now = d.injected_now;

@@ -51,6 +51,16 @@ __device__ __forceinline__ int32_t* start_buf(const Ctx& c, int sel) {
 }
 __device__ __forceinline__ bool gated_off(const int32_t* gate) { return gate && *gate == 0; }
 
+// Sharded mode (shard.py): lanes are own, halo (ghost copies imported from
+// their owner after every step) or outside the zone.
+enum : uint8_t { ZF_OWN = 1, ZF_HALO = 2, ZF_EXACT = 4 };
+// Snapshot range [x, y) of lane L: its CSR segment, or for a halo lane its
+// ghost range (ghosts live after the snapshot's own records, same buffer).
+__device__ __forceinline__ int2 seg(const Ctx& c, const int32_t* S, int32_t L) {
+  if (c.sharded && (c.zone[L] & ZF_HALO)) return c.ghost_seg[L];
+  return make_int2(S[L], S[L + 1]);
+}
+
 // Conditional graph nodes (engine.cu issue_step): a section of the step graph
 // runs only when its deciding kernel sets the handle.  The handles default to
 // 0 at every graph launch; in eager launches (profiling, host-continuation
@@ -209,7 +219,8 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #endif
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   Dyn* dy = c.dyn;
-  const int32_t n = dy->n_a;
+  const int32_t n_a = dy->n_a;
+  const int32_t n = n_a + (c.sharded ? dy->n_g : 0);
   const VRec* A = c.lay[dy->cur];
   const int32_t* S = c.start[dy->cur];
   const Params& p = c.p;
@@ -219,8 +230,20 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   for (int32_t i = gtid(); i < n; i += gstride()) {
     const VRec me = A[i];
     const int32_t snap_lane = me.lane;
+    bool ghost = false;
+    if (c.sharded) {
+      // records of non-own lanes in the snapshot proper are last step's
+      // local copies (superseded by the imported ghosts): drop them
+      if (i < n_a && !(c.zone[snap_lane] & ZF_OWN)) {
+        c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
+        c.stay[i] = 0;
+        continue;
+      }
+      ghost = i >= n_a;
+    }
     const LaneRec L0 = c.lanes[snap_lane];
-    const int32_t lo0 = S[snap_lane], hi0 = S[snap_lane + 1];
+    const int2 sg0 = seg(c, S, snap_lane);
+    const int32_t lo0 = sg0.x, hi0 = sg0.y;
     const int32_t* roads = c.routes + me.rptr;  // roads[0] = current road, roads[1] = next (or -1)
     const int32_t next_road = __ldg(roads + 1);
     const double v = me.v;
@@ -293,7 +316,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           const LaneRec LN = c.lanes[nb];
           if (!mandatory && !any && conn_from_id(c, nb, next_road) < 0) continue;
           const double s_t = me.s * (LN.len / L0.len);
-          const int32_t lo = S[nb], hi = S[nb + 1];
+          const int2 sgn = seg(c, S, nb);
+          const int32_t lo = sgn.x, hi = sgn.y;
           const int32_t m = count_above(A, lo, hi, s_t);
           const int32_t tl_i = m > 0 ? lo + m - 1 : -1;
           const View tl = view_at(A, tl_i);
@@ -345,7 +369,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     double gap = CUDART_INF, lead_v = 0.0;
     bool found = false;
     if (!have_final) {
-      int32_t lo = S[lane], hi = S[lane + 1];
+      const int2 sgl = seg(c, S, lane);
+      const int32_t lo = sgl.x, hi = sgl.y;
       if (hi > lo) {
         int32_t ld = -1;
         if (!changed) {
@@ -410,7 +435,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
             rq += 1;
             if (!(c.lflag[nxt] & LF_OPEN)) break;
           }
-          const int32_t lo = S[nxt], hi = S[nxt + 1];
+          const int2 sgx = seg(c, S, nxt);
+          const int32_t lo = sgx.x, hi = sgx.y;
           if (hi > lo) {
             const VRec rear = A[hi - 1];
             double g = dist + rear.s - Lv;
@@ -478,7 +504,10 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       }
     }
     VRec out{ns, nv, me.vix, nptr, nl, i};
-    if (arrived) {
+    if (arrived && ghost) {  // the owner records it
+      out.lane = -1;
+      c.stay[i] = 0;
+    } else if (arrived) {
       out.lane = -1;
       c.stay[i] = 0;
       c.status[me.vix] = TSB_STATUS_FINISHED;
@@ -499,6 +528,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       }
     } else {
       count_bucket(c, nl, snap_lane, i);
+      if (ghost && (c.zone[nl] & ZF_OWN)) c.status[me.vix] = TSB_STATUS_DRIVING;  // entered an own lane
     }
     c.B[i] = out;
   }
@@ -527,8 +557,8 @@ __global__ void k_count_hostq(Ctx c) {
 // status words carry the invocation's epoch, so stale words from earlier
 // steps are ignored and the step graph needs no memset nodes.  All ntiles
 // blocks must be launched and draw a ticket (the gate is grid-uniform).
-static constexpr int SCAN_SITES = 4;
-enum { SCAN_LANES = 0, SCAN_INJ_LANES = 1, SCAN_INJ_RETRY = 2, SCAN_REGROUP = 3 };
+static constexpr int SCAN_SITES = 6;
+enum { SCAN_LANES = 0, SCAN_INJ_LANES = 1, SCAN_INJ_RETRY = 2, SCAN_REGROUP = 3, SCAN_EXPORT = 4, SCAN_IMPORT = 5 };
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in, int32_t* out, int out_sel,
                                              const int32_t* n_dev, int32_t n_static, int32_t ntiles,
@@ -779,7 +809,7 @@ __global__ void k_place(Ctx c) {
     dy->n_c = CS[c.n_lanes];
     if (dy->n_hostq > 0 && !c.split) dy->overflow |= 4;
   }
-  const int32_t n = dy->n_a;
+  const int32_t n = dy->n_a + (c.sharded ? dy->n_g : 0);
   const int lid = threadIdx.x & 31;
   // one pass, whole warps (the ballots below need all 32 lanes)
   for (int32_t base = (gtid() >> 5) << 5; base < n; base += gstride()) {
@@ -799,7 +829,7 @@ __global__ void k_place(Ctx c) {
     // rank among the lane's stayers: stayers ahead of j in its snapshot
     // segment [a0, j) -- inside this warp from the ballot, before it by a
     // short loop (only for the warp's first segment)
-    const int32_t a0 = SA[L];
+    const int32_t a0 = seg(c, SA, L).x;
     const int lo_lane = a0 > base ? a0 - base : 0;
     const unsigned below = (1u << lid) - 1u, from = ~((1u << lo_lane) - 1u);
     int32_t rank = __popc(stay_bits & below & from);
@@ -1122,6 +1152,7 @@ __device__ int32_t resolve_lane(const Ctx& c, VRec* C, const int32_t* CS, const 
 
 // State of one replay (a component, or everything in the sequential path).
 struct Replay {
+  int32_t zf;  // sharded: zone flags seen (1 = an own lane, 2 = an inexact lane)
   int32_t* heap;
   int32_t hn;
   int32_t reach;
@@ -1148,6 +1179,7 @@ __device__ void replay(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, 
           c.rs_touched[x] = 1;
           R.touched[R.nt++] = x;
         }
+        if (c.sharded) R.zf |= ((c.zone[x] & ZF_OWN) ? 1 : 0) | ((c.zone[x] & ZF_EXACT) ? 0 : 2);
         if (x > R.reach) R.reach = x;
         L = x;
         break;
@@ -1376,6 +1408,21 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
     const int32_t k = c.comp_id[lab[i]];
     c.comp_ev[atomicAdd(&c.comp_fill[k], 1)] = cl[i];
   }
+  if (c.sharded) {
+    // a chain that can change an own lane must stay inside lanes this rank
+    // computes exactly (shard.py); otherwise fail loudly
+    for (int32_t k = threadIdx.x; k < nc; k += blockDim.x) c.comp_flags[k] = 0;
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint8_t z = c.zone[cl[i]];
+      const int32_t k = c.comp_id[lab[i]];
+      if (z & ZF_OWN) atomicOr(&c.comp_flags[k], 1);
+      if (!(z & ZF_EXACT)) atomicOr(&c.comp_flags[k], 2);
+    }
+    __syncthreads();
+    for (int32_t k = threadIdx.x; k < nc; k += blockDim.x)
+      if (c.comp_flags[k] == 3) dy->overflow |= 16;
+  }
   if (threadIdx.x == 0) dy->n_comp = nc;
 }
 
@@ -1394,7 +1441,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
   const VRec* A = c.lay[dy->cur];
   const int64_t max_reverts = (int64_t)dy->n_c + 2;
   for (int32_t k = blockIdx.x * RC_WARPS + w; k < nc; k += gridDim.x * RC_WARPS) {
-    Replay R{sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
+    Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
     if (lid == 0)
       for (int32_t q = c.comp_off[k]; q < c.comp_off[k + 1]; q++) {
         const int32_t L = c.comp_ev[q];
@@ -1427,7 +1474,7 @@ __global__ void __launch_bounds__(32) k_resolve(Ctx c) {
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
   const VRec* A = c.lay[dy->cur];
-  Replay R{c.rs_heap, 0, -1, c.rs_moved, 0, c.rs_touched_list, 0, 0};
+  Replay R{0, c.rs_heap, 0, -1, c.rs_moved, 0, c.rs_touched_list, 0, 0};
   if (lid == 0) {
     dy->n_moved = 0;
     dy->reverts_last = 0;
@@ -1449,6 +1496,9 @@ __global__ void __launch_bounds__(32) k_resolve(Ctx c) {
     dy->n_moved = R.nmoved;
     dy->reverts_last = R.reverts;
     dy->resolve_sequential += 1;
+    // conservative in sharded mode (no component split here): an own lane and
+    // an inexact lane in the same replay
+    if (c.sharded && R.zf == 3) dy->overflow |= 16;
   }
 }
 
@@ -1533,7 +1583,7 @@ __global__ void k_inject_due(Ctx c) {
   const int32_t nr = dy->n_retry;
   if (threadIdx.x == 0) {
     const int32_t lo = dy->pend_ptr;
-    int32_t a = lo, b = c.n_trips;
+    int32_t a = lo, b = c.n_pend;
     const double t = dy->time;
     while (a < b) {  // pending departures are non-decreasing
       int32_t m = (a + b) >> 1;
@@ -1837,7 +1887,8 @@ __global__ void k_patch_finish(Ctx c) {
     dy->finished_total += dy->finished_now;
     dy->reverts_total += dy->reverts_last;
     dy->fin_log_n += dy->finished_now;
-    dy->speeds_pending = 1;  // accumulated by the next k_update or a flush
+    dy->speeds_pending = 1;  // accumulated by the next step's k_speeds branch or a flush
+    dy->n_own = 0;           // sharded: recounted by k_count_own
   }
 }
 
@@ -1868,6 +1919,7 @@ __global__ void k_speeds(Ctx c, int flush) {
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int32_t r = gtid() >> 5; r < c.n_roads; r += warps) {
     const int2 span = c.road_span[r];
+    if (c.sharded && !(c.zone[span.x] & ZF_OWN)) continue;  // the owner accumulates it
     const int32_t j0 = S[span.x], j1 = S[span.y + 1];
     if (j1 == j0) continue;
     double sum = 0.0;
@@ -1887,7 +1939,7 @@ __global__ void k_speeds_done(Ctx c) { c.dyn->speeds_pending = 0; }
 
 __global__ void k_begin_step(Ctx c) {
   Dyn* dy = c.dyn;
-  dy->vehicle_updates += dy->n_a;
+  dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_a;
   dy->finished_now = 0;
   dy->n_events = 0;
   dy->complex = 0;
@@ -1927,6 +1979,96 @@ __global__ void k_min_gap(Ctx c, double* out) {
     best = fmin(best, sm[0]);
     *out = best;
   }
+}
+
+
+// ------------------------------------------------------------------ sharded exchange
+//
+// Message of rank r to peer q (bytes): int32 counts of r's export lanes for q
+// (ascending lane ids, shard.py), padded to 32 B, then the lanes' vehicle
+// records (VRec, lane-sorted as in r's snapshot).  The receiver appends them
+// to its snapshot as ghosts and points its halo lanes at them.
+
+__device__ __forceinline__ int64_t align32(int64_t x) { return (x + 31) & ~(int64_t)31; }
+
+// Own vehicles in the snapshot (vehicle_updates counts them next step).
+__global__ void k_count_own(Ctx c) {
+  Dyn* dy = c.dyn;
+  const int32_t* S = c.start[dy->cur];
+  int32_t mine = 0;
+  for (int32_t L = gtid(); L < c.n_lanes; L += gstride())
+    if (c.zone[L] & ZF_OWN) mine += S[L + 1] - S[L];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&dy->n_own, mine);
+}
+
+__global__ void k_exp_count(Ctx c) {
+  const int32_t* S = c.start[c.dyn->cur];
+  for (int32_t e = gtid(); e < c.n_exp; e += gstride()) {
+    const int32_t L = c.exp_lane[e];
+    c.exp_cnt[e] = S[L + 1] - S[L];
+  }
+}
+
+// Byte offset of peer q's message in the send buffer.
+__device__ __forceinline__ int64_t exp_base(const Ctx& c, int q) {
+  int64_t b = 0;
+  for (int p = 0; p < q; p++) {
+    const int64_t e0 = c.peer_first_exp[p], e1 = c.peer_first_exp[p + 1];
+    b += align32(4 * (e1 - e0)) + 32 * (int64_t)(c.exp_pos[e1] - c.exp_pos[e0]);
+  }
+  return b;
+}
+
+// Warp per export entry: header count and records.
+__global__ void k_exp_pack(Ctx c, uint8_t* send) {
+  const VRec* A = c.lay[c.dyn->cur];
+  const int32_t* S = c.start[c.dyn->cur];
+  const int lid = threadIdx.x & 31;
+  for (int32_t e = gtid() >> 5; e < c.n_exp; e += gstride() >> 5) {
+    const int q = c.exp_peer[e];
+    const int64_t e0 = c.peer_first_exp[q];
+    const int64_t base = exp_base(c, q);
+    const int32_t L = c.exp_lane[e];
+    const int32_t n = c.exp_cnt[e];
+    if (lid == 0) ((int32_t*)(send + base))[e - e0] = n;
+    VRec* dst = (VRec*)(send + base + align32(4 * (c.peer_first_exp[q + 1] - e0))) + (c.exp_pos[e] - c.exp_pos[e0]);
+    for (int32_t k = lid; k < n; k += 32) dst[k] = A[S[L] + k];
+  }
+}
+
+// Receive side: counts from the headers (src_base[q] = byte offset of
+// source q's message in the receive buffer).
+struct SrcBase {
+  int64_t b[9];
+};
+__global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
+  for (int32_t e = gtid(); e < c.n_imp; e += gstride()) {
+    const int q = c.imp_peer[e];
+    c.imp_cnt[e] = ((const int32_t*)(recv + sb.b[q]))[e - c.peer_first_imp[q]];
+  }
+}
+
+// Warp per import entry: ghost range of the lane, records appended after the
+// snapshot's own records.
+__global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
+  Dyn* dy = c.dyn;
+  VRec* A = c.lay[dy->cur];
+  const int32_t base = dy->n_a;
+  const int lid = threadIdx.x & 31;
+  for (int32_t e = gtid() >> 5; e < c.n_imp; e += gstride() >> 5) {
+    const int q = c.imp_peer[e];
+    const int64_t e0 = c.peer_first_imp[q];
+    const int32_t L = c.imp_lane[e];
+    const int32_t n = c.imp_cnt[e];
+    const VRec* src = (const VRec*)(recv + sb.b[q] + align32(4 * (c.peer_first_imp[q + 1] - e0))) +
+                      (c.imp_pos[e] - c.imp_pos[e0]);
+    const int32_t at = base + c.imp_pos[e];
+    if (lid == 0) c.ghost_seg[L] = make_int2(at, at + n);
+    for (int32_t k = lid; k < n; k += 32) A[at + k] = src[k];
+  }
+  if (gtid() == 0) dy->n_g = c.imp_pos[c.n_imp];
 }
 
 }  // namespace tsb

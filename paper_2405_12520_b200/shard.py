@@ -1,0 +1,182 @@
+"""Lane partitioning and halo zones for the sharded (multi-GPU) engine.
+
+SURVEY.md 8(e): the road graph is split into spatial bands of junctions; a
+connector belongs to its junction's rank and a road (all its lanes) to the
+rank of its upstream junction.  Each rank then simulates its own lanes plus a
+halo of foreign lanes (an overlapping decomposition), so that everything
+that can influence its own lanes within ONE step is computed locally from
+exact inputs:
+
+* reads of the update (world.py:261-397): the lane, its road siblings (MOBIL)
+  and the lanes within `lookahead` downstream (_sense);
+* vehicles that can enter an own lane in one step (transitions, lane
+  changes) -- lanes within one step's travel upstream;
+* revert partners (world.py:501-559): lanes own vehicles can enter, whose
+  sweep may send them back.
+
+After every step each rank sends the vehicles of its own lanes that lie in a
+neighbour's halo to that neighbour (one all-to-all of boundary lanes); the
+neighbour uses them as read-only ghosts for the next step.  Lanes marked
+EXACT are those whose post-step content is computed exactly; the engine
+checks at run time that every revert chain touching an own lane stays inside
+EXACT lanes and fails loudly otherwise (never silently wrong).
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+
+from .flat import KIND_CONNECTOR, KIND_ROAD, FlatNet
+
+ZONE_OWN, ZONE_HALO, ZONE_EXACT = 1, 2, 4
+
+
+@dataclass
+class ShardPlan:
+    rank: int
+    nranks: int
+    lane_owner: np.ndarray   # int32 per lane (-1 for id holes)
+    zone: np.ndarray         # uint8 per lane: OWN | HALO, EXACT
+    export_lanes: list       # per destination rank: own lanes in its halo (ascending)
+    import_lanes: list       # per source rank: its lanes in my halo (ascending)
+
+
+def lane_owners(flat: FlatNet, junc_pos: np.ndarray, nranks: int) -> np.ndarray:
+    """Bands of junctions sorted by (y, x), balanced by lane count."""
+    nj = len(flat.junction_ids)
+    n = flat.n_lanes
+    # a road's upstream junction: the junction of its predecessor connectors
+    # (else its successors'); all lanes of a road share it
+    road_junc = np.full(len(flat.road_ids), -1, dtype=np.int64)
+    for r in range(len(flat.road_ids)):
+        for lane in flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]]:
+            preds = flat.pred[flat.pred_off[lane]:flat.pred_off[lane + 1]]
+            conns = [int(p) for p in preds if flat.lane_kind[p] == KIND_CONNECTOR]
+            if conns:
+                road_junc[r] = flat.lane_junction[conns[0]]
+                break
+        if road_junc[r] < 0:
+            for lane in flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]]:
+                succ = flat.succ[flat.succ_off[lane]:flat.succ_off[lane + 1]]
+                conns = [int(s) for s in succ if flat.lane_kind[s] == KIND_CONNECTOR]
+                if conns:
+                    road_junc[r] = flat.lane_junction[conns[0]]
+                    break
+        if road_junc[r] < 0:
+            road_junc[r] = 0
+    lane_junc = np.full(n, -1, dtype=np.int64)
+    is_conn = flat.lane_kind == KIND_CONNECTOR
+    lane_junc[is_conn] = flat.lane_junction[is_conn]
+    is_road = flat.lane_kind == KIND_ROAD
+    lane_junc[is_road] = road_junc[flat.lane_road[is_road]]
+    weight = np.bincount(lane_junc[lane_junc >= 0], minlength=nj).astype(np.float64)
+    order = np.lexsort((junc_pos[:, 0], junc_pos[:, 1]))  # by y, then x
+    cum = np.cumsum(weight[order])
+    total = cum[-1] if len(cum) else 0.0
+    band = np.minimum((cum - weight[order] * 0.5) * nranks // max(total, 1.0), nranks - 1).astype(np.int32)
+    junc_rank = np.empty(nj, dtype=np.int32)
+    junc_rank[order] = band
+    owner = np.full(n, -1, dtype=np.int32)
+    ok = lane_junc >= 0
+    owner[ok] = junc_rank[lane_junc[ok]]
+    return owner
+
+
+def _csr_lists(off, idx, n):
+    return [idx[off[i]:off[i + 1]] for i in range(n)]
+
+
+def _reach(flat: FlatNet, seeds, dist: float, downstream: bool) -> set:
+    """Lanes whose near end lies within `dist` of a seed's boundary, walking
+    successors from the seeds' ends (downstream) or predecessors from their
+    starts (upstream).  The distance to a lane is the length of the lanes
+    strictly between it and the seed."""
+    off, idx = (flat.succ_off, flat.succ) if downstream else (flat.pred_off, flat.pred)
+    best: dict[int, float] = {}
+    dq = deque((int(s), -1.0) for s in seeds)
+    while dq:
+        lane, d = dq.popleft()
+        base = 0.0 if d < 0 else d + float(flat.lane_len[lane])
+        if base >= dist:
+            continue
+        for nb in idx[off[lane]:off[lane + 1]]:
+            nb = int(nb)
+            if flat.lane_kind[nb] < 0:
+                continue
+            if nb not in best or best[nb] > base:
+                best[nb] = base
+                dq.append((nb, base))
+    return set(best)
+
+
+def _siblings(flat: FlatNet, lanes: set) -> set:
+    out = set(lanes)
+    for lane in lanes:
+        if flat.lane_kind[lane] == KIND_ROAD:
+            r = flat.lane_road[lane]
+            out.update(int(x) for x in flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]])
+    return out
+
+
+def max_step_travel(flat: FlatNet, config) -> float:
+    """Upper bound of one vehicle's displacement in one step (m)."""
+    vmax = max(float(config.idm.v0), float(flat.lane_cap[flat.lane_kind >= 0].max(initial=0.0)))
+    return vmax * config.dt + 0.5 * config.idm.a_max * config.dt * config.dt + 1.0
+
+
+def plan_shard(flat: FlatNet, owner: np.ndarray, rank: int, nranks: int, config) -> ShardPlan:
+    n = flat.n_lanes
+    travel = max_step_travel(flat, config)
+    own = set(int(x) for x in np.nonzero(owner == rank)[0])
+
+    def down(seeds, dist):
+        return _reach(flat, seeds, dist, downstream=True)
+
+    def up(seeds, dist):
+        return _reach(flat, seeds, dist, downstream=False)
+
+    # lanes own vehicles may enter (revert partners) and lanes that may feed them
+    near = _siblings(flat, own | down(own, 2 * travel))
+    feed = _siblings(flat, near | up(near, 2 * travel))
+    # everything those vehicles read: downstream lookahead from anywhere on the lane
+    zone_set = _siblings(flat, feed | down(feed, config.lookahead + travel))
+    zone = np.zeros(n, dtype=np.uint8)
+    for lane in zone_set:
+        zone[lane] = ZONE_OWN if owner[lane] == rank else ZONE_HALO
+    for lane in own:
+        zone[lane] = ZONE_OWN
+    # exact_update(L): L's siblings and its downstream reads are in the zone
+    in_zone = zone > 0
+    exact_update = np.zeros(n, dtype=bool)
+    for lane in zone_set | own:
+        sib = _siblings(flat, {lane})
+        reads = down({lane}, config.lookahead + travel)
+        exact_update[lane] = all(in_zone[x] for x in sib | reads)
+    # exact_lane(H): every lane whose vehicles can end in H this step is exact_update
+    for lane in zone_set | own:
+        src = _siblings(flat, {lane}) | up({lane}, travel)
+        if all(exact_update[x] for x in src if flat.lane_kind[x] >= 0):
+            zone[lane] |= ZONE_EXACT
+    export_lanes, import_lanes = [], []
+    for q in range(nranks):
+        if q == rank:
+            export_lanes.append(np.zeros(0, dtype=np.int32))
+            import_lanes.append(np.zeros(0, dtype=np.int32))
+            continue
+        export_lanes.append(None)
+        import_lanes.append(np.array(sorted(x for x in zone_set if owner[x] == q and zone[x] & ZONE_HALO),
+                                     dtype=np.int32))
+    return ShardPlan(rank, nranks, owner, zone, export_lanes, import_lanes)
+
+
+def plan_all(flat: FlatNet, junc_pos: np.ndarray, nranks: int, config) -> list[ShardPlan]:
+    """Plans for every rank (export lists are the peers' import lists)."""
+    owner = lane_owners(flat, junc_pos, nranks)
+    plans = [plan_shard(flat, owner, r, nranks, config) for r in range(nranks)]
+    for r, p in enumerate(plans):
+        p.export_lanes = [plans[q].import_lanes[r] if q != r else np.zeros(0, dtype=np.int32)
+                          for q in range(nranks)]
+    return plans

@@ -1,0 +1,151 @@
+"""Multi-GPU engine: one process per GPU, lanes partitioned into spatial bands.
+
+SURVEY.md 8(e).  Every rank builds the same network, trips and routes (the
+inputs are replicated; they are small next to the vehicle state), owns the
+lanes of its band (shard.py) and simulates them plus a halo of ghost lanes.
+One step on rank r is
+
+1. the single-GPU step graph over own + ghost vehicles (csrc/kernels.cu): the
+   update of ghosts reproduces exactly what their owner computes for every
+   vehicle that can affect an own lane this step (transitions into own lanes,
+   revert partners); chains that would leave the exactly-computed zone make
+   the engine fail loudly (TSB_ECAP), never silently diverge;
+2. one exchange: each rank packs the vehicles of its own lanes that lie in a
+   peer's halo (tsb_shard_export, device buffers) and the peers' packets
+   become its ghosts for the next step (tsb_shard_import).  The transfer is
+   `torch.distributed.all_to_all_single` on device tensors -- NCCL over
+   NVLink/NVSwitch on a multi-GPU node; gloo with host staging for tests;
+3. step counters (driving, waiting, finished, ...) are summed over ranks.
+
+Vehicles migrate implicitly: a vehicle that crosses into a peer's band was a
+ghost there, so the peer already holds its exact new state.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native, shard
+from .cabi import TsbReport, pack_network, pack_params, pack_shard, pack_trips
+from .errors import InputError
+from .flat import FlatNet, FlatTrips, flatten_network, flatten_trips
+from .params import EngineConfig
+
+RECORD_BYTES = 32
+
+
+class ShardedWorld:
+    """One rank of the sharded engine (call collectively on every rank)."""
+
+    def __init__(self, flat: FlatNet, ft: FlatTrips, junc_pos: np.ndarray, config: EngineConfig | None,
+                 seed: int, rank: int, nranks: int, device: int = 0, group=None, host_staging: bool = False):
+        import torch
+        import torch.distributed as dist
+
+        self.config = config or EngineConfig()
+        self.config.validate()
+        self.rank, self.nranks = rank, nranks
+        self.group = group
+        self.dist = dist
+        self.torch = torch
+        self.host_staging = host_staging
+        self.flat, self.ft = flat, ft
+        self.plan = shard.plan_all(flat, junc_pos, nranks, self.config)[rank]
+        pn, pt, ps = pack_network(flat), pack_trips(ft), pack_shard(self.plan)
+        params = pack_params(self.config, seed, pow_mode=0)
+        h = C.c_void_p()
+        _native.check(_native.lib().tsb_create_sharded(C.byref(pn.struct), C.byref(pt.struct), C.byref(params),
+                                                       device, C.byref(ps.struct), C.byref(h)))
+        self._h = h
+        self._report = TsbReport()
+        self.device = torch.device("cuda", device)
+        # a packet holds at most every vehicle (32 B) plus one int32 count per lane entry
+        n_exp = sum(len(x) for x in self.plan.export_lanes)
+        n_imp = sum(len(x) for x in self.plan.import_lanes)
+        self._send = torch.zeros(len(ft.ids) * RECORD_BYTES + 4 * n_exp + 32 * nranks + 64, dtype=torch.uint8,
+                                 device=self.device)
+        self._recv = torch.zeros(len(ft.ids) * RECORD_BYTES + 4 * n_imp + 32 * nranks + 64, dtype=torch.uint8,
+                                 device=self.device)
+        self.exchanged_bytes = 0
+        self._exchange()  # initial ghosts (empty network: zero vehicles)
+
+    @classmethod
+    def from_network(cls, net, trips, config=None, seed=0, rank=0, nranks=1, device=0, group=None,
+                     host_staging=False):
+        config = config or EngineConfig()
+        flat = flatten_network(net, config.controller)
+        ft = flatten_trips(flat, trips)
+        jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64).reshape(-1, 2)
+        return cls(flat, ft, jp, config, seed, rank, nranks, device, group, host_staging)
+
+    def close(self):
+        if self._h is not None:
+            _native.lib().tsb_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # ------------------------------------------------------------ exchange
+
+    def _exchange(self):
+        torch, dist = self.torch, self.dist
+        out_b = np.zeros(self.nranks, dtype=np.int64)
+        _native.check(_native.lib().tsb_shard_export(self._h, C.c_void_p(self._send.data_ptr()),
+                                                     self._send.numel(), out_b.ctypes.data))
+        sizes_out = torch.tensor(out_b, dtype=torch.int64)
+        sizes_in = torch.zeros(self.nranks, dtype=torch.int64)
+        if not self.host_staging:
+            sizes_out, sizes_in = sizes_out.to(self.device), sizes_in.to(self.device)
+        dist.all_to_all_single(sizes_in, sizes_out, group=self.group)
+        in_b = sizes_in.cpu().numpy().astype(np.int64)
+        n_out, n_in = int(out_b.sum()), int(in_b.sum())
+        if n_in > self._recv.numel():
+            raise InputError("receive buffer too small")
+        send, recv = self._send[:n_out], self._recv[:n_in]
+        if self.host_staging:  # gloo: exchange through host memory
+            send_h, recv_h = send.cpu(), torch.zeros(n_in, dtype=torch.uint8)
+            dist.all_to_all_single(recv_h, send_h, in_b.tolist(), out_b.tolist(), group=self.group)
+            recv.copy_(recv_h)
+        else:
+            dist.all_to_all_single(recv, send, in_b.tolist(), out_b.tolist(), group=self.group)
+        torch.cuda.current_stream(self.device).synchronize()
+        self.exchanged_bytes += n_out
+        _native.check(_native.lib().tsb_shard_import(self._h, C.c_void_p(self._recv.data_ptr()), in_b.ctypes.data))
+
+    # ------------------------------------------------------------ stepping
+
+    def step_local(self, n: int = 1):
+        """n steps, exchanging ghosts after each (no global reductions)."""
+        for _ in range(n):
+            _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
+            self._exchange()
+
+    def report(self) -> dict:
+        """StepReport counters summed over ranks (time and step are shared)."""
+        torch, dist = self.torch, self.dist
+        r = self._report
+        keys = ("driving", "waiting", "finished", "dropped", "injected_now", "finished_now", "vehicle_updates")
+        t = torch.tensor([getattr(r, k) for k in keys], dtype=torch.int64)
+        if not self.host_staging:
+            t = t.to(self.device)
+        dist.all_reduce(t, group=self.group)
+        out = dict(zip(keys, (int(x) for x in t.cpu().tolist())))
+        out["time"] = r.time
+        return out
+
+    def own_state(self):
+        """This rank's own vehicles, lane-sorted: dict of arrays (vix, lane, road_pos, s, v)."""
+        n = max(len(self.ft.ids), 1)
+        nd = C.c_int32()
+        ls = np.zeros(self.flat.n_lanes + 1, dtype=np.int32)
+        out = {k: np.zeros(2 * n, dtype=t) for k, t in (("vix", np.int32), ("lane", np.int32),
+                                                         ("road_pos", np.int32), ("s", np.float64),
+                                                         ("v", np.float64))}
+        _native.check(_native.lib().tsb_state(self._h, C.byref(nd), ls.ctypes.data, out["vix"].ctypes.data,
+                                              out["lane"].ctypes.data, out["road_pos"].ctypes.data,
+                                              out["s"].ctypes.data, out["v"].ctypes.data))
+        m = nd.value
+        own = (self.plan.zone[out["lane"][:m]] & shard.ZONE_OWN) > 0
+        return {k: a[:m][own] for k, a in out.items()}

@@ -1,0 +1,29 @@
+"""Sharded engine (2-3 ranks, may share one GPU) against the single-GPU engine:
+every StepReport counter summed over ranks, and every rank's own lanes
+bit-identical (membership, order, road_pos, s, v) every 10 steps."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(name, steps, nproc, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "dist", "shard_worker.py"), name, str(steps)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    line = [x for x in out.stdout.splitlines() if x.startswith("SHARD_RESULT")]
+    assert line, out.stdout[-3000:] + out.stderr[-3000:]
+    print(line[0])
+    assert "mismatches=0" in line[0], out.stdout[-3000:]
+
+
+@pytest.mark.parametrize("name,steps,nproc,port", [("grid6x2", 300, 2, 29611), ("dense", 200, 2, 29612),
+                                                   ("grid8x3", 300, 3, 29613)])
+def test_sharded_equals_single(name, steps, nproc, port):
+    _run(name, steps, nproc, port)
