@@ -9,9 +9,11 @@ start (world.py:663).  Construction and the first (bulk injection) step are
 excluded, as in the reference's `trafficsim bench` (cli.py:482-489).
 
 Arms:
-  default           the B200 engine (one CUDA graph per step), N ranks =
-                    N independent replicas (weak scaling, "replicas only"
-                    until the sharded path lands)
+  default           the B200 engine (one CUDA graph per step).  Under torchrun
+                    with N > 1 ranks: the sharded engine (sharded.py) -- the
+                    same 1M-vehicle network split into N spatial lane bands,
+                    one GPU each, ghost lanes exchanged every step with an
+                    NCCL all-to-all (strong scaling: total work fixed)
   --impl reference  the reference algorithm on the host CPU: the C port in
                     oracle/ (the reference itself is pure Python and cannot
                     travel to the GPU box), rank 0 only.
@@ -57,6 +59,78 @@ def build_workload(n_vehicles: int, spacing: float):
     router.close()
     ft = flatten_trips(flat, trips)
     return net, flat, trips, ft
+
+
+def run_sharded(args, ws, rank, local, pg, workload):
+    """N > 1: the sharded engine on one GPU per rank (strong scaling)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2405_12520_b200 import EngineConfig, _native
+    from paper_2405_12520_b200.sharded import ShardedWorld
+
+    net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
+    jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    sw = ShardedWorld(flat, ft, jp, EngineConfig(), 42, rank, ws, device=local,
+                      host_staging=os.environ.get("TSB_BENCH_GLOO") == "1")
+    L = _native.lib()
+    sw.step_local(1)  # bulk injection (excluded)
+    with ClockSampler(local) as clk:
+        sw.step_local(args.warmup)
+        u0 = sw.report()["vehicle_updates"]
+        barrier(pg)
+        torch.cuda.synchronize()
+        _native.check(L.tsb_mark(sw._h, 0))
+        sw.step_local(args.steps)
+        _native.check(L.tsb_mark(sw._h, 1))
+        ms = C.c_double()
+        _native.check(L.tsb_marks_elapsed(sw._h, 0, 1, C.byref(ms)))
+        torch.cuda.synchronize()
+        barrier(pg)
+        u1 = sw.report()["vehicle_updates"]
+        # end to end: the public per-step call plus the summed StepReport read back
+        e2e_steps = max(10, args.steps // 4)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            sw.step_local(1)
+            rep = sw.report()
+        e2e_dt = allreduce_max(pg, time.perf_counter() - t0)
+        u2 = rep["vehicle_updates"]
+    clocks = clk.summary()
+    t_max = allreduce_max(pg, ms.value)
+    updates = u1 - u0
+    value = updates / (t_max / 1e3)
+    hbm, peak_src = load_peaks()
+    own = int((sw.plan.zone & 1).sum())
+    halo = int(((sw.plan.zone & 2) > 0).sum())
+    xbytes = sw.exchanged_bytes
+    sw.close()
+    if rank != 0:
+        return
+    per_gpu = value / ws
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "vehicles_total": args.vehicles, "lanes": flat.n_lanes,
+                   "parallelism": f"lane bands x{ws} (sharded.py; halo lanes rank0: {halo} vs own {own})",
+                   "exchange": "per step: NCCL all_to_all_single of boundary-lane packets + counters",
+                   "exchanged_bytes_rank0_total": xbytes,
+                   "timing": "engine-stream events around K steps incl. exchanges, max over ranks"},
+        "e2e": {"value": (u2 - u1) / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 8 * 7,
+                "how": "ShardedWorld.step_local + all-reduced StepReport per step, wall clock, max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": B_ALG * per_gpu / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": B_ALG * per_gpu / 1e9 / hbm, "traffic": None, "kernel": "whole step per GPU",
+                     "peak_source": peak_src,
+                     "alg_bytes": f"{B_ALG} B/vehicle-update x updates per GPU per second"},
+        "cpu_baseline": None,
+        "clocks": clocks,
+        "gpu_launches": None,
+    }
+    print(json.dumps(line), flush=True)
 
 
 class ClockSampler:
@@ -125,6 +199,9 @@ def cpu_baseline(net, flat, trips, warm: int, sample_steps: int, threads: int):
 
 
 def dist_setup():
+    """torchrun environment -> (world size, rank, local rank, process group).
+    TSB_BENCH_GLOO=1 (functional test on one GPU): gloo, every rank on cuda:0,
+    exchange staged through host memory."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -133,10 +210,18 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if os.environ.get("TSB_BENCH_GLOO") == "1":
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
         pg = dist
     return ws, rank, local, pg
+
+
+def _red_device():
+    return "cpu" if os.environ.get("TSB_BENCH_GLOO") == "1" else "cuda"
 
 
 def allreduce_max(pg, x: float) -> float:
@@ -144,7 +229,7 @@ def allreduce_max(pg, x: float) -> float:
         return x
     import torch
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_red_device())
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -154,7 +239,7 @@ def allreduce_sum(pg, x: float) -> float:
         return x
     import torch
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_red_device())
     pg.all_reduce(t, op=pg.ReduceOp.SUM)
     return float(t.item())
 
@@ -193,7 +278,7 @@ def main():
         line = {
             "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": n_gpus,
             "steps": k, "warmup": min(args.warmup, 3), "ms_per_step": 1000.0 * dt / k,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload, "parallelism": f"cpu-{cores}-threads"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{k} steps x {args.vehicles} vehicles after injection + warm-up; "
@@ -203,6 +288,10 @@ def main():
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
+        return
+
+    if ws > 1:
+        run_sharded(args, ws, rank, local, pg, workload)
         return
 
     import ctypes as C
@@ -277,7 +366,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "vehicles_per_gpu": n_drv, "lanes": flat.n_lanes,
                    "parallelism": f"replicas x{n_gpus}" if n_gpus > 1 else "single",
                    "l2": "no flush: per-step working set (4 x 32 MB vehicle layouts + route gathers + "

@@ -188,6 +188,10 @@ int tsb_profile_steps(tsb_engine* e, int32_t n_steps, int32_t cap, double* kerne
 const char* tsb_kernel_name(int32_t k);
 /* Device time (ms) of n graph-replayed steps bracketed by CUDA events. */
 int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms);
+/* Timing marks on the engine stream (slots 0..7): record, then elapsed ms
+ * between two recorded marks (waits for the later one). */
+int tsb_mark(tsb_engine* e, int32_t slot);
+int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
 /* Test knobs: bit 0 forces the sequential revert-chain resolver, bit 1 the
  * full (non-incremental) regroup.  Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);

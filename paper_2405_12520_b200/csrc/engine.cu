@@ -90,6 +90,7 @@ struct tsb_engine {
   cudaStream_t body = nullptr;  // captures conditional-section bodies
   cudaStream_t side = nullptr;  // parallel branch (road aggregate)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
@@ -993,6 +994,8 @@ void tsb_destroy(tsb_engine* e) {
   if (e->body) cudaStreamDestroy(e->body);
   if (e->side) cudaStreamDestroy(e->side);
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+  for (auto& m : e->marks)
+    if (m) cudaEventDestroy(m);
   if (e->ev_join) cudaEventDestroy(e->ev_join);
   delete e;
 }
@@ -1237,6 +1240,23 @@ int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   RC(sync_dyn(e));
+  return TSB_OK;
+}
+
+int tsb_mark(tsb_engine* e, int32_t slot) {
+  if (!e || slot < 0 || slot >= 8) return fail(TSB_EINVAL, "mark slot out of range");
+  if (!e->marks[slot]) CK(cudaEventCreate(&e->marks[slot]));
+  CK(cudaEventRecord(e->marks[slot], e->stream));
+  return TSB_OK;
+}
+
+int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms) {
+  if (!e || a < 0 || a >= 8 || b < 0 || b >= 8 || !e->marks[a] || !e->marks[b])
+    return fail(TSB_EINVAL, "marks not recorded");
+  CK(cudaEventSynchronize(e->marks[b]));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, e->marks[a], e->marks[b]));
+  *ms = f;
   return TSB_OK;
 }
 

@@ -36,6 +36,34 @@ from .params import EngineConfig
 RECORD_BYTES = 32
 
 
+def alltoall_packets(send, out_bytes: np.ndarray, recv, group=None, host_staging: bool = False):
+    """Variable-size all-to-all of byte packets: send[:sum(out_bytes)] holds
+    the packets for ranks 0..N-1 back to back; returns (received bytes, the
+    per-source sizes).  Device tensors go through NCCL; with host_staging the
+    bytes travel through host memory (gloo, tests)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = send.device
+    sizes_out = torch.tensor(out_bytes, dtype=torch.int64)
+    sizes_in = torch.zeros(len(out_bytes), dtype=torch.int64)
+    if not host_staging and dev.type == "cuda":
+        sizes_out, sizes_in = sizes_out.to(dev), sizes_in.to(dev)
+    dist.all_to_all_single(sizes_in, sizes_out, group=group)
+    in_b = sizes_in.cpu().numpy().astype(np.int64)
+    n_out, n_in = int(out_bytes.sum()), int(in_b.sum())
+    if n_in > recv.numel():
+        raise InputError("receive buffer too small")
+    s, r = send[:n_out], recv[:n_in]
+    if host_staging and dev.type == "cuda":
+        r_h = torch.zeros(n_in, dtype=torch.uint8)
+        dist.all_to_all_single(r_h, s.cpu(), in_b.tolist(), out_bytes.tolist(), group=group)
+        r.copy_(r_h)
+    else:
+        dist.all_to_all_single(r, s, in_b.tolist(), out_bytes.tolist(), group=group)
+    return r, in_b
+
+
 class ShardedWorld:
     """One rank of the sharded engine (call collectively on every rank)."""
 
@@ -90,28 +118,13 @@ class ShardedWorld:
     # ------------------------------------------------------------ exchange
 
     def _exchange(self):
-        torch, dist = self.torch, self.dist
+        torch = self.torch
         out_b = np.zeros(self.nranks, dtype=np.int64)
         _native.check(_native.lib().tsb_shard_export(self._h, C.c_void_p(self._send.data_ptr()),
                                                      self._send.numel(), out_b.ctypes.data))
-        sizes_out = torch.tensor(out_b, dtype=torch.int64)
-        sizes_in = torch.zeros(self.nranks, dtype=torch.int64)
-        if not self.host_staging:
-            sizes_out, sizes_in = sizes_out.to(self.device), sizes_in.to(self.device)
-        dist.all_to_all_single(sizes_in, sizes_out, group=self.group)
-        in_b = sizes_in.cpu().numpy().astype(np.int64)
-        n_out, n_in = int(out_b.sum()), int(in_b.sum())
-        if n_in > self._recv.numel():
-            raise InputError("receive buffer too small")
-        send, recv = self._send[:n_out], self._recv[:n_in]
-        if self.host_staging:  # gloo: exchange through host memory
-            send_h, recv_h = send.cpu(), torch.zeros(n_in, dtype=torch.uint8)
-            dist.all_to_all_single(recv_h, send_h, in_b.tolist(), out_b.tolist(), group=self.group)
-            recv.copy_(recv_h)
-        else:
-            dist.all_to_all_single(recv, send, in_b.tolist(), out_b.tolist(), group=self.group)
+        _, in_b = alltoall_packets(self._send, out_b, self._recv, self.group, self.host_staging)
         torch.cuda.current_stream(self.device).synchronize()
-        self.exchanged_bytes += n_out
+        self.exchanged_bytes += int(out_b.sum())
         _native.check(_native.lib().tsb_shard_import(self._h, C.c_void_p(self._recv.data_ptr()), in_b.ctypes.data))
 
     # ------------------------------------------------------------ stepping

@@ -1,0 +1,81 @@
+"""Host-side logic of the sharded engine (CPU): the lane partition and the
+halo zones (paper_2405_12520_b200/shard.py) and the packet transport over a
+real 2-rank gloo process group."""
+
+from __future__ import annotations
+
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2405_12520_b200 import EngineConfig, generate_grid, make_ring
+from paper_2405_12520_b200 import shard
+from paper_2405_12520_b200.flat import KIND_CONNECTOR, KIND_ROAD, flatten_network
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _plans(net, n):
+    flat = flatten_network(net)
+    jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    return flat, shard.plan_all(flat, jp, n, EngineConfig())
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_partition_covers_lanes_and_keeps_roads_whole(n):
+    flat, plans = _plans(generate_grid(6, 6, lanes_per_direction=2), n)
+    owner = plans[0].lane_owner
+    valid = flat.lane_kind >= 0
+    assert np.all(owner[valid] >= 0) and np.all(owner[valid] < n)
+    for r in range(len(flat.road_ids)):
+        lanes = flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]]
+        assert len(set(owner[lanes].tolist())) == 1
+    counts = np.bincount(owner[valid], minlength=n)
+    assert counts.min() > 0.5 * counts.mean()  # balanced bands
+    for p in plans:
+        own = (p.zone & shard.ZONE_OWN) > 0
+        assert np.array_equal(own, owner == p.rank)
+        assert np.all(p.zone[own] & shard.ZONE_EXACT)  # own lanes are computed exactly
+
+
+def test_halo_holds_lookahead_and_feeders():
+    net = generate_grid(6, 6, lanes_per_direction=2)
+    flat, plans = _plans(net, 2)
+    cfg = EngineConfig()
+    travel = shard.max_step_travel(flat, cfg)
+    for p in plans:
+        own = set(np.nonzero(p.lane_owner == p.rank)[0].tolist())
+        zone = p.zone > 0
+        reads = shard._reach(flat, own, cfg.lookahead + travel, downstream=True)
+        feeders = shard._reach(flat, own, travel, downstream=False)
+        assert all(zone[x] for x in reads | feeders)
+
+
+def test_export_import_lists_are_mutual():
+    flat, plans = _plans(generate_grid(8, 8, lanes_per_direction=3), 4)
+    for p in plans:
+        for q in range(4):
+            assert np.array_equal(p.export_lanes[q], plans[q].import_lanes[p.rank])
+            if q != p.rank:
+                imp = plans[q].import_lanes[p.rank]
+                assert np.all(p.lane_owner[imp] == p.rank)
+                assert np.all(plans[q].zone[imp] & shard.ZONE_HALO)
+
+
+def test_ring_two_ranks():
+    net = make_ring(40, radius=40 * 200.0 / (2 * math.pi))
+    flat, plans = _plans(net, 2)
+    assert all(len(p.import_lanes[1 - p.rank]) > 0 for p in plans)
+
+
+def test_packet_transport_two_ranks_gloo():
+    """alltoall_packets (the engine's exchange) on a 2-process gloo group."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29631",
+           os.path.join(ROOT, "tests", "dist", "transport_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert "TRANSPORT_OK 2" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
