@@ -819,33 +819,51 @@ __global__ void k_place(Ctx c) {
     const bool st = valid && c.stay[j];
     const unsigned stay_bits = __ballot_sync(0xffffffffu, st);
     const int32_t L = r.lane;
-    if (!valid || L < 0) continue;  // arrived (no ballots follow)
-    if (!st) {
-      const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + atomicAdd(&c.ent_cur[L], 1);
-      C[pos] = r;
-      flag_lane(c, L);
-      continue;
-    }
-    // rank among the lane's stayers: stayers ahead of j in its snapshot
-    // segment [a0, j) -- inside this warp from the ballot, before it by a
-    // short loop (only for the warp's first segment)
-    const int32_t a0 = seg(c, SA, L).x;
-    const int lo_lane = a0 > base ? a0 - base : 0;
-    const unsigned below = (1u << lid) - 1u, from = ~((1u << lo_lane) - 1u);
-    int32_t rank = __popc(stay_bits & below & from);
-    int32_t k = -1;  // previous stayer
-    const unsigned prev_bits = stay_bits & below & from;
-    if (prev_bits) k = base + 31 - __clz(prev_bits);
-    for (int32_t q = base - 1; q >= a0; q--) {
-      if (c.stay[q]) {
-        rank++;
-        if (k < 0) k = q;
+    bool flag = false;  // this lane needs k_lanefix
+    if (L >= 0) {
+      if (!st) {
+        const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + atomicAdd(&c.ent_cur[L], 1);
+        C[pos] = r;
+        flag = true;
+      } else {
+        // rank among the lane's stayers: stayers ahead of j in its snapshot
+        // segment [a0, j) -- inside this warp from the ballot, before it by a
+        // short loop (only for the warp's first segment)
+        const int32_t a0 = seg(c, SA, L).x;
+        const int lo_lane = a0 > base ? a0 - base : 0;
+        const unsigned below = (1u << lid) - 1u, from = ~((1u << lo_lane) - 1u);
+        int32_t rank = __popc(stay_bits & below & from);
+        int32_t k = -1;  // previous stayer
+        const unsigned prev_bits = stay_bits & below & from;
+        if (prev_bits) k = base + 31 - __clz(prev_bits);
+        for (int32_t q = base - 1; q >= a0; q--) {
+          if (c.stay[q]) {
+            rank++;
+            if (k < 0) k = q;
+          }
+        }
+        C[CS[L] + rank] = r;
+        if (k >= 0) {
+          const VRec pr = c.B[k];
+          flag = !ahead_of(pr.s, pr.vix, r.s, r.vix) || r.s > ((pr.s - p.L) - p.s0_floor) + 1e-12;
+        }
       }
     }
-    C[CS[L] + rank] = r;
-    if (k >= 0) {
-      const VRec pr = c.B[k];
-      if (!ahead_of(pr.s, pr.vix, r.s, r.vix) || r.s > ((pr.s - p.L) - p.s0_floor) + 1e-12) flag_lane(c, L);
+    // warp-aggregated append of newly flagged lanes: one flag atomic per lane
+    // per warp (jammed lanes flag every vehicle), one counter atomic per warp
+    const unsigned fm = __ballot_sync(0xffffffffu, flag);
+    bool first_flag = false;
+    if (flag) {
+      const unsigned grp = __match_any_sync(fm, L);
+      if (lid == __ffs(grp) - 1) first_flag = atomicExch(&c.fix_flag[L], 1) == 0;
+    }
+    const unsigned fb = __ballot_sync(0xffffffffu, first_flag);
+    if (fb) {
+      int32_t slot0 = 0;
+      const int leader = __ffs(fb) - 1;
+      if (lid == leader) slot0 = atomicAdd(&dy->n_fix, __popc(fb));
+      slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+      if (first_flag) c.fix_list[slot0 + __popc(fb & ((1u << lid) - 1))] = L;
     }
   }
 }
