@@ -209,7 +209,7 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #define UPD_BT 256
 #endif
 #ifndef UPD_MINB
-#define UPD_MINB 3
+#define UPD_MINB 4
 #endif
 // One thread per vehicle (grid = ceil(N / BT) blocks, scheduled dynamically)
 // instead of a grid-stride loop: the last partial wave of a grid-stride
@@ -1265,6 +1265,40 @@ __device__ void replay_finish(const Ctx& c, const Replay& R) {
   for (int32_t q = 0; q < R.nmoved; q++) c.rs_reverted[R.moved[q]] = 0;
 }
 
+// In-place exclusive scan of a[0, n) in shared memory, n <= 2 * blockDim.x;
+// returns the total.  Every thread of the block calls.
+__device__ int32_t block_excl_scan2(int32_t* a, int n) {
+  __shared__ int32_t ws[32];
+  const int t = threadIdx.x, lid = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
+  const int i0 = 2 * t, i1 = 2 * t + 1;
+  const int32_t x0 = i0 < n ? a[i0] : 0, x1 = i1 < n ? a[i1] : 0;
+  const int32_t sum = x0 + x1;
+  int32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lid >= o) incl += y;
+  }
+  if (lid == 31) ws[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int32_t v = lid < nw ? ws[lid] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lid >= o) v += y;
+    }
+    ws[lid] = v;
+  }
+  __syncthreads();
+  const int32_t base = (w ? ws[w - 1] : 0) + incl - sum;
+  if (i0 < n) a[i0] = base;
+  if (i1 < n) a[i1] = base + x0;
+  const int32_t total = ws[nw - 1];
+  __syncthreads();
+  return total;
+}
+
 // Closure of the event lanes under "entered member -> its snapshot lane",
 // split into components (one CTA).  Output: dy->n_comp components, comp_off
 // / comp_ev (event lanes per component), comp_size; or dy->complex = 1 when
@@ -1386,44 +1420,45 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
     __syncthreads();
   }
   // component ids (roots in index order), sizes, events per component
-  if (threadIdx.x == 0) {
-    int32_t nc = 0;
-    for (int32_t i = 0; i < n; i++)
-      if (lab[i] == i) c.comp_id[i] = nc++;
-    s_ncomp = nc;
-    for (int32_t k = 0; k <= nc; k++) c.comp_off[k] = 0;
-  }
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) indeg[i] = lab[i] == i ? 1 : 0;
   __syncthreads();
-  const int32_t nc = s_ncomp;
-  for (int32_t k = threadIdx.x; k < nc; k += blockDim.x) {
+  const int32_t nc = block_excl_scan2(indeg, n);  // indeg[root] = component id
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) c.comp_id[i] = indeg[lab[i]];
+  for (int32_t k = threadIdx.x; k <= nc; k += blockDim.x) {
     c.comp_size[k] = 0;
     c.comp_edges[k] = 0;
+    c.comp_off[k] = 0;
   }
   __syncthreads();
   for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const int32_t k = c.comp_id[lab[i]];
+    const int32_t k = c.comp_id[i];
     atomicAdd(&c.comp_size[k], 1);
-    if (i < ne) atomicAdd(&c.comp_off[k + 1], 1);
+    if (i < ne) atomicAdd(&c.comp_off[k], 1);
   }
   for (int32_t e = threadIdx.x; e < nedge; e += blockDim.x)
-    atomicAdd(&c.comp_edges[c.comp_id[lab[c.cl_idx[eu[e]] - 1]]], 1);
+    atomicAdd(&c.comp_edges[c.comp_id[c.cl_idx[eu[e]] - 1]], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int32_t k = 0; k < nc; k++) {
-      c.comp_off[k + 1] += c.comp_off[k];
-      // heap / touched lists hold distinct lanes; each revert moves a
-      // distinct entered member (an edge)
-      if (c.comp_size[k] > HCAP || c.comp_edges[k] > 2 * HCAP) s_over = 1;
-    }
-    for (int32_t k = 0; k < nc; k++) c.comp_fill[k] = c.comp_off[k];
+  // event offsets per component (scan in shared memory; eu is free now)
+  for (int32_t k = threadIdx.x; k < nc; k += blockDim.x) {
+    eu[k] = c.comp_off[k];
+    // heap / touched lists hold distinct lanes; each revert moves a
+    // distinct entered member (an edge)
+    if (c.comp_size[k] > HCAP || c.comp_edges[k] > 2 * HCAP) s_over = 1;
   }
+  __syncthreads();
+  const int32_t tot_ev = block_excl_scan2(eu, nc);
+  for (int32_t k = threadIdx.x; k < nc; k += blockDim.x) {
+    c.comp_off[k] = eu[k];
+    c.comp_fill[k] = eu[k];
+  }
+  if (threadIdx.x == 0) c.comp_off[nc] = tot_ev;
   __syncthreads();
   if (s_over) {
     if (threadIdx.x == 0) dy->complex = 1;
     return;
   }
   for (int32_t i = threadIdx.x; i < ne; i += blockDim.x) {
-    const int32_t k = c.comp_id[lab[i]];
+    const int32_t k = c.comp_id[i];
     c.comp_ev[atomicAdd(&c.comp_fill[k], 1)] = cl[i];
   }
   if (c.sharded) {
@@ -1433,7 +1468,7 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
     __syncthreads();
     for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
       const uint8_t z = c.zone[cl[i]];
-      const int32_t k = c.comp_id[lab[i]];
+      const int32_t k = c.comp_id[i];
       if (z & ZF_OWN) atomicOr(&c.comp_flags[k], 1);
       if (!(z & ZF_EXACT)) atomicOr(&c.comp_flags[k], 2);
     }
