@@ -90,7 +90,8 @@ typedef struct tsb_params {
   double mobil_politeness, mobil_threshold, mobil_b_safe, mobil_eval_prob;
   double vehicle_length, speed_window, amber, s0_floor, mp_interval, mp_min_green;
   int32_t controller; /* 0 = fixed, 1 = max_pressure */
-  int32_t pow_mode;   /* 0 = correctly-rounded powers (device) */
+  int32_t pow_mode;   /* 1 = glibc pow() bit for bit, as CPython's `**` (default);
+                       * 0 = correctly rounded powers.  See DESIGN.md. */
   uint64_t seed;
 } tsb_params;
 
@@ -188,6 +189,8 @@ int tsb_profile_steps(tsb_engine* e, int32_t n_steps, int32_t cap, double* kerne
 const char* tsb_kernel_name(int32_t k);
 /* Device time (ms) of n graph-replayed steps bracketed by CUDA events. */
 int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms);
+/* Switch the power arithmetic between steps (tsb_params.pow_mode). */
+int tsb_set_pow_mode(tsb_engine* e, int32_t pow_mode);
 /* Timing marks on the engine stream (slots 0..7): record, then elapsed ms
  * between two recorded marks (waits for the later one). */
 int tsb_mark(tsb_engine* e, int32_t slot);

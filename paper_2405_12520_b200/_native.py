@@ -48,6 +48,7 @@ SIGNATURES = {
     "tsb_set_debug": (_i32, [_vp, _i32]),
     "tsb_create_sharded": (_i32, [_vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
     "tsb_mark": (_i32, [_vp, _i32]),
+    "tsb_set_pow_mode": (_i32, [_vp, _i32]),
     "tsb_marks_elapsed": (_i32, [_vp, _i32, _i32, C.POINTER(_f64)]),
     "tsb_shard_export": (_i32, [_vp, _vp, _i64, _vp]),
     "tsb_shard_import": (_i32, [_vp, _vp, _vp]),

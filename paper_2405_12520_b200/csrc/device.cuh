@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "../../include/tsb200.h"
+#include "pow_glibc.cuh"
 
 namespace tsb {
 
@@ -129,6 +130,7 @@ struct Params {
   uint64_t rng_h2;   // keyed-RNG fold state after (seed, STREAM_MOBIL): constant for the run
   int32_t controller;
   int32_t delta_int; // delta as an integer power if integral in [1, 64], else 0
+  int32_t pow_glibc; // 1: powers exactly as glibc's pow (CPython `**`); 0: correctly rounded
   uint64_t seed;
 };
 
@@ -170,7 +172,7 @@ struct Ctx {
   int32_t* cnt;
   int32_t* cursor;
   int32_t* ent;      // per lane: movers entering it this step
-  int32_t* ent_cur;
+  int32_t* mslot;    // per B record (movers): slot among the new lane's entrants
   uint8_t* stay;     // per B record: still on its snapshot lane
   int32_t* fix_flag;
   int32_t* fix_list;
@@ -303,6 +305,7 @@ __device__ __forceinline__ double div_pos(double x, double y) {
 // Free-road term (v / v0_eff)**delta (idm.py:24-25).
 __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_eff) {
   const double x = div_pos(v, v0_eff);
+  if (p.pow_glibc) return glibc_pow::pow(x, p.delta);
   return p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
 }
 
@@ -318,7 +321,7 @@ __device__ __forceinline__ double idm_with_free(const Params& p, double fr, doub
   double g = free_road ? 1.0 : gap;
   asm("mov.b64 %0, %0;" : "+d"(g));
   const double q = div_pos(s_star, g);
-  const double inter = free_road ? 0.0 : q * q;
+  const double inter = free_road ? 0.0 : (p.pow_glibc ? glibc_pow::pow(q, 2.0) : q * q);
   return p.a_max * (1.0 - fr - inter);
 }
 

@@ -636,8 +636,8 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   if (sh && (sh->nranks < 1 || sh->nranks > 8 || sh->rank < 0 || sh->rank >= sh->nranks || !sh->zone))
     return fail(TSB_EINVAL, "bad shard description (1 <= nranks <= 8)");
   if (sh && p->controller != 0) return fail(TSB_EINVAL, "sharded mode supports fixed-time signals only");
-  if (p->pow_mode != 0)
-    return fail(TSB_EINVAL, "pow_mode %d unsupported on device (0 = correctly rounded powers)", p->pow_mode);
+  if (p->pow_mode != 0 && p->pow_mode != 1)
+    return fail(TSB_EINVAL, "pow_mode %d unsupported (0 = correctly rounded, 1 = glibc pow)", p->pow_mode);
   auto e = std::make_unique<tsb_engine>();
   e->device = device;
   CK(cudaSetDevice(device));
@@ -695,6 +695,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
                     ? (int32_t)p->idm_delta
                     : 0;
   P.seed = p->seed;
+  P.pow_glibc = p->pow_mode == 1 ? 1 : 0;
 
   // lanes
   e->lanes.resize(NL);
@@ -852,7 +853,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.cnt, NL));
   RC(dalloc(E, &c.cursor, NL));
   RC(dalloc(E, &c.ent, NL));
-  RC(dalloc(E, &c.ent_cur, NL));
+  RC(dalloc(E, &c.mslot, CAP));
   RC(dalloc(E, &c.stay, CAP));
   RC(dalloc(E, &c.fix_flag, NL));
   RC(dalloc(E, &c.fix_list, NL));
@@ -1240,6 +1241,13 @@ int tsb_time_steps(tsb_engine* e, int32_t n_steps, double* ms) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   RC(sync_dyn(e));
+  return TSB_OK;
+}
+
+int tsb_set_pow_mode(tsb_engine* e, int32_t pow_mode) {
+  if (!e || (pow_mode != 0 && pow_mode != 1)) return fail(TSB_EINVAL, "pow_mode must be 0 or 1");
+  e->c.p.pow_glibc = pow_mode;
+  e->graph_dirty = true;  // Params are captured by value in the step graph
   return TSB_OK;
 }
 

@@ -184,9 +184,11 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
 
 // Post-update lane counts for the C layout; a vehicle that left its snapshot
 // lane is also a "mover" (k_place_movers / k_lanefix).
+// A mover's slot among its new lane's entrants comes from the same atomic
+// (k_place then needs no atomic of its own).
 __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t snap_lane, int32_t i) {
   atomicAdd(&c.cnt[lane], 1);
-  if (lane != snap_lane) atomicAdd(&c.ent[lane], 1);
+  if (lane != snap_lane) c.mslot[i] = atomicAdd(&c.ent[lane], 1);
   c.stay[i] = lane == snap_lane ? 1 : 0;
 }
 
@@ -822,7 +824,7 @@ __global__ void k_place(Ctx c) {
     bool flag = false;  // this lane needs k_lanefix
     if (L >= 0) {
       if (!st) {
-        const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + atomicAdd(&c.ent_cur[L], 1);
+        const int32_t pos = CS[L] + (c.cnt[L] - c.ent[L]) + c.mslot[j];
         C[pos] = r;
         flag = true;
       } else {
@@ -887,7 +889,6 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
     if (lid == 0) {
       c.fix_flag[L] = 0;
       c.ent[L] = 0;  // consumed: zero for the next step (no memsets)
-      c.ent_cur[L] = 0;
     }
     const bool on_chip = n <= LX_CAP;
     VRec* in = on_chip ? s_in[w] : c.D + lo;  // oversized lanes stage in D

@@ -68,7 +68,8 @@ class ShardedWorld:
     """One rank of the sharded engine (call collectively on every rank)."""
 
     def __init__(self, flat: FlatNet, ft: FlatTrips, junc_pos: np.ndarray, config: EngineConfig | None,
-                 seed: int, rank: int, nranks: int, device: int = 0, group=None, host_staging: bool = False):
+                 seed: int, rank: int, nranks: int, device: int = 0, group=None, host_staging: bool = False,
+                 pow_mode: int = 1):
         import torch
         import torch.distributed as dist
 
@@ -82,7 +83,7 @@ class ShardedWorld:
         self.flat, self.ft = flat, ft
         self.plan = shard.plan_all(flat, junc_pos, nranks, self.config)[rank]
         pn, pt, ps = pack_network(flat), pack_trips(ft), pack_shard(self.plan)
-        params = pack_params(self.config, seed, pow_mode=0)
+        params = pack_params(self.config, seed, pow_mode=pow_mode)
         h = C.c_void_p()
         _native.check(_native.lib().tsb_create_sharded(C.byref(pn.struct), C.byref(pt.struct), C.byref(params),
                                                        device, C.byref(ps.struct), C.byref(h)))

@@ -35,6 +35,10 @@ FINISHED = "finished"
 DROPPED = "dropped"
 _STATUS = {0: WAITING, 1: DRIVING, 2: FINISHED, 3: DROPPED}
 _INT32_MAX = 2**31 - 1
+# IDM powers (idm.py:25, idm.py:30): POW_GLIBC evaluates them exactly as
+# glibc's pow() -- what CPython's `**` calls -- so trajectories are bit-identical
+# to the reference's; POW_CORRECT rounds them correctly.
+POW_CORRECT, POW_GLIBC = 0, 1
 
 
 @dataclass(frozen=True)
@@ -80,7 +84,8 @@ class World:
     """B200 engine behind the reference ``World`` interface."""
 
     def __init__(self, net, trips, config: EngineConfig | None = None, seed: int = 0,
-                 device: int = 0, _flat: FlatNet | None = None, _flat_trips: FlatTrips | None = None):
+                 device: int = 0, _flat: FlatNet | None = None, _flat_trips: FlatTrips | None = None,
+                 pow_mode: int = POW_GLIBC):
         config = config or EngineConfig()
         config.validate()
         self.net = net
@@ -92,7 +97,8 @@ class World:
         self._h = None
         packed_net = pack_network(self._flat)
         packed_trips = pack_trips(self._ft)
-        params = pack_params(config, seed, pow_mode=0)
+        params = pack_params(config, seed, pow_mode=pow_mode)
+        self.pow_mode = pow_mode
         h = C.c_void_p()
         _native.check(_native.lib().tsb_create(C.byref(packed_net.struct), C.byref(packed_trips.struct),
                                                C.byref(params), device, C.byref(h)))
@@ -109,9 +115,10 @@ class World:
 
     @classmethod
     def from_flat(cls, flat: FlatNet, flat_trips: FlatTrips, config: EngineConfig | None = None,
-                  seed: int = 0, device: int = 0) -> "World":
+                  seed: int = 0, device: int = 0, pow_mode: int = None) -> "World":
         """Construct from pre-flattened inputs (large synthetic configs)."""
-        return cls(None, None, config, seed, device, _flat=flat, _flat_trips=flat_trips)
+        return cls(None, None, config, seed, device, _flat=flat, _flat_trips=flat_trips,
+                   pow_mode=POW_GLIBC if pow_mode is None else pow_mode)
 
     # ------------------------------------------------------------ lifecycle
 

@@ -33,12 +33,14 @@ def compare_reports(gpu: World, ref: OracleWorld, step: int):
         assert getattr(g, k) == getattr(r, k), f"step {step}: report.{k} {getattr(g, k)} vs {getattr(r, k)}"
 
 
-def run_pair(net, trips, config, seed, steps, exact=True, every=1, check_signals=True, debug=0):
-    gpu = World(net, trips, config, seed=seed)
+def run_pair(net, trips, config, seed, steps, exact=True, every=1, check_signals=True, debug=0, pow_mode=1):
+    """GPU engine and CPU oracle in the same power arithmetic (1: glibc pow,
+    what the reference computes; 0: correctly rounded), compared bit for bit."""
+    gpu = World(net, trips, config, seed=seed, pow_mode=pow_mode)
     if debug:
         from paper_2405_12520_b200 import _native
         _native.check(_native.lib().tsb_set_debug(gpu._h, debug))
-    ref = OracleWorld(net, trips, config, seed=seed, pow_mode=0 if exact else 1)
+    ref = OracleWorld(net, trips, config, seed=seed, pow_mode=pow_mode)
     reverts = 0
     try:
         for k in range(1, steps + 1):

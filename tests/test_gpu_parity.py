@@ -42,17 +42,19 @@ def test_grid44_single_lane():
     _close(g, r)
 
 
-def test_grid44_two_lanes_mobil():
+@pytest.mark.parametrize("pow_mode", [1, 0])
+def test_grid44_two_lanes_mobil(pow_mode):
     net = generate_grid(4, 4, lanes_per_direction=2)
     trips = random_trips(net, 2500, seed=42, window=(0.0, 700.0))
-    g, r, reverts = run_pair(net, trips, EngineConfig(), 42, 1000, every=10)
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 42, 1000, every=10, pow_mode=pow_mode)
     _close(g, r)
 
 
-def test_jammed_grid_reverts():
+@pytest.mark.parametrize("pow_mode", [1, 0])
+def test_jammed_grid_reverts(pow_mode):
     net = generate_grid(4, 4)
     trips = random_trips(net, 3000, seed=11, window=(0.0, 300.0))
-    g, r, reverts = run_pair(net, trips, EngineConfig(), 11, 500, every=5)
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 11, 500, every=5, pow_mode=pow_mode)
     _close(g, r)
 
 
