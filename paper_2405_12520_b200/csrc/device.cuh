@@ -303,9 +303,12 @@ __device__ __forceinline__ double div_pos(double x, double y) {
 }
 
 // Free-road term (v / v0_eff)**delta (idm.py:24-25).
+// G: glibc-pow arithmetic (compile-time, so each k_update instantiation only
+// carries the code of its own mode).
+template <bool G>
 __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_eff) {
   const double x = div_pos(v, v0_eff);
-  if (p.pow_glibc) return glibc_pow::pow(x, p.delta);
+  if (G) return glibc_pow::pow(x, p.delta);
   return p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
 }
 
@@ -314,6 +317,7 @@ __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_
 // The interaction division is evaluated with a dummy divisor on a free road
 // (gap == inf): the compiler speculates it past the branch, and s*/inf == 0
 // would take the division slow path for every leaderless vehicle.
+template <bool G>
 __device__ __forceinline__ double idm_with_free(const Params& p, double fr, double v, double dv, double gap) {
   const bool free_road = isinf(gap);
   const double vdv = v * dv;
@@ -321,20 +325,22 @@ __device__ __forceinline__ double idm_with_free(const Params& p, double fr, doub
   double g = free_road ? 1.0 : gap;
   asm("mov.b64 %0, %0;" : "+d"(g));
   const double q = div_pos(s_star, g);
-  const double inter = free_road ? 0.0 : (p.pow_glibc ? glibc_pow::pow(q, 2.0) : q * q);
+  const double inter = free_road ? 0.0 : (G ? glibc_pow::pow(q, 2.0) : q * q);
   return p.a_max * (1.0 - fr - inter);
 }
 
 // idm_with_free for a gap that may be <= 0 where the caller discards the
 // result (branch-free MOBIL evaluation): a safe divisor keeps the division
 // on its fast path; for gap > 0 it is the same expression, bit for bit.
+template <bool G>
 __device__ __forceinline__ double idm_safe(const Params& p, double fr, double v, double dv, double gap) {
-  return idm_with_free(p, fr, v, dv, gap > 0.0 ? gap : 1.0);
+  return idm_with_free<G>(p, fr, v, dv, gap > 0.0 ? gap : 1.0);
 }
 
 // idm.py:17-31.
+template <bool G>
 __device__ __forceinline__ double idm_accel(const Params& p, double v, double dv, double gap, double v_cap) {
-  return idm_with_free(p, idm_free(p, v, py_min(p.v0, v_cap)), v, dv, gap);
+  return idm_with_free<G>(p, idm_free<G>(p, v, py_min(p.v0, v_cap)), v, dv, gap);
 }
 
 // rng.py:24-41: splitmix64 finaliser fold over (seed, stream, id, step).

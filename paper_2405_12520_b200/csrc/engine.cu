@@ -214,7 +214,10 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     L.post();
     cudaEventRecord(e->ev_join, e->side);
     cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
-    LAUNCH(KC_UPDATE, k_update, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+    if (c.p.pow_glibc)
+      LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+    else
+      LAUNCH(KC_UPDATE, k_update<false>, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);

@@ -219,6 +219,7 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #ifndef UPD_GRID_CAP
 #define UPD_GRID_CAP (1 << 30)
 #endif
+template <bool G>
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   Dyn* dy = c.dyn;
   const int32_t n_a = dy->n_a;
@@ -299,12 +300,12 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         const double g_of_old = me.s - Lv - cf.s;
         const double g_of_new = gap_to(cl, cf.s, Lv);
         const bool of_ok = cf.ok && g_of_old > 0.0 && g_of_new > 0.0;
-        fr_me = idm_free(p, v, v0e_cur);
+        fr_me = idm_free<G>(p, v, v0e_cur);
         have_fr_me = true;
-        const double fr_cf = idm_free(p, cf.v, v0e_cur);
-        const double a_me_x = idm_safe(p, fr_me, v, dv_to(v, cl), g_cur);
-        const double a_of_x = idm_safe(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
-        const double a_of_new_x = idm_safe(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
+        const double fr_cf = idm_free<G>(p, cf.v, v0e_cur);
+        const double a_me_x = idm_safe<G>(p, fr_me, v, dv_to(v, cl), g_cur);
+        const double a_of_x = idm_safe<G>(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
+        const double a_of_new_x = idm_safe<G>(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
         const double a_me = (g_cur <= 0.0) ? -CUDART_INF : a_me_x;
         const double a_of = of_ok ? a_of_x : 0.0;
         const double a_of_new = of_ok ? a_of_new_x : 0.0;
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           const double g_nf_old = gap_to(tl, tf.s, Lv);
           if (g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0)) continue;
           const double v0e_tgt = py_min(p.v0, LN.cap);
-          const double fr_me_t = (v0e_tgt == v0e_cur) ? fr_me : idm_free(p, v, v0e_tgt);
-          const double fr_tf = idm_free(p, tf.v, v0e_tgt);
-          const double a_me_new = idm_safe(p, fr_me_t, v, dv_to(v, tl), g_tl);
-          const double a_nf_x = idm_safe(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
-          const double a_nf_new_x = idm_safe(p, fr_tf, tf.v, tf.v - v, g_tf);  // new leader: me at s_t
+          const double fr_me_t = (v0e_tgt == v0e_cur) ? fr_me : idm_free<G>(p, v, v0e_tgt);
+          const double fr_tf = idm_free<G>(p, tf.v, v0e_tgt);
+          const double a_me_new = idm_safe<G>(p, fr_me_t, v, dv_to(v, tl), g_tl);
+          const double a_nf_x = idm_safe<G>(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
+          const double a_nf_new_x = idm_safe<G>(p, fr_tf, tf.v, tf.v - v, g_tf);  // new leader: me at s_t
           const double a_nf = tf.ok ? a_nf_x : 0.0;
           const double a_nf_new = tf.ok ? a_nf_new_x : 0.0;
           if (tf.ok && a_nf_new < -p.b_safe) continue;
@@ -459,8 +460,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       a = a_final;
     } else {
       const double v0e = py_min(p.v0, L1.cap);
-      const double fr = (have_fr_me && v0e == v0e_cur) ? fr_me : idm_free(p, v, v0e);
-      a = idm_with_free(p, fr, v, v - lead_v, gap);
+      const double fr = (have_fr_me && v0e == v0e_cur) ? fr_me : idm_free<G>(p, v, v0e);
+      a = idm_with_free<G>(p, fr, v, v - lead_v, gap);
     }
     const double dt = p.dt;
     double v_new = v + a * dt, disp;
