@@ -90,6 +90,8 @@ struct tsb_engine {
   cudaStream_t body = nullptr;  // captures conditional-section bodies
   cudaStream_t side = nullptr;  // parallel branch (road aggregate)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr;  // parallel branch (signals, clock, due list)
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
   bool capturing = false;
@@ -225,20 +227,39 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   scan(e, L, KC_SCAN, SCAN_LANES, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
   LAUNCH(KC_SCATTER, k_place, vgrid, VB, c);
   LAUNCH(KC_LANESORT_SWEEP, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
+  // Fixed-time signals, the clock and the due list do not depend on vehicle
+  // positions: with a fixed-time controller they run on a parallel branch
+  // beside the revert resolution (joined before the injection section).
+  const bool fork_signals = c.p.controller == 0;
+  if (fork_signals) {
+    cudaEventRecord(e->ev_fork2, e->cur);
+    cudaStreamWaitEvent(e->side2, e->ev_fork2, 0);
+    cudaStream_t main_s = e->cur;
+    e->cur = e->side2;
+    LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
+    LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+    LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
+    cudaEventRecord(e->ev_join2, e->side2);
+    e->cur = main_s;
+  }
   // exact revert resolution (only when some lane's sweep reverts)
   LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
   cond_begin(e, COND_RESOLVE);
   LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
   cond_end(e);
-  if (c.p.controller == 1) {
-    cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->cur);
-    LAUNCH(KC_SIGNALS, k_lane_counts, vgrid, VB, c);
+  if (!fork_signals) {
+    if (c.p.controller == 1) {  // max-pressure reads the post-sweep lane counts
+      cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->cur);
+      LAUNCH(KC_SIGNALS, k_lane_counts, vgrid, VB, c);
+    }
+    LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
+    LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+    LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
+  } else {
+    cudaStreamWaitEvent(e->cur, e->ev_join2, 0);
   }
-  LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
-  LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
   // injection (only when trips are due or waiting for a retry)
-  LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
   cond_begin(e, COND_INJECT);
   LAUNCH(KC_INJECT, k_inject_hist, vgrid, VB, c);
   scan(e, L, KC_INJECT, SCAN_INJ_LANES, c.inj_cnt, c.inj_start, SEL_NONE, nullptr, NL, NL, &dy->n_due);
@@ -256,7 +277,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   cond_begin(e, COND_PATCH);
   LAUNCH(KC_REGROUP, k_patch_starts, tgrid, VB, c);
   LAUNCH(KC_REGROUP, k_patch_copy, vgrid, VB, c);
-  LAUNCH(KC_REGROUP, k_patch_dirty, 64, VB, c);
+  LAUNCH(KC_REGROUP, k_patch_dirty, 296, 32 * PD_WARPS, c);
   cond_end(e);
   cond_begin(e, COND_FULL);
   cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
@@ -647,6 +668,9 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->body, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->ev_fork2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
   e->cur = e->stream;
@@ -997,6 +1021,9 @@ void tsb_destroy(tsb_engine* e) {
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->body) cudaStreamDestroy(e->body);
   if (e->side) cudaStreamDestroy(e->side);
+  if (e->side2) cudaStreamDestroy(e->side2);
+  if (e->ev_fork2) cudaEventDestroy(e->ev_fork2);
+  if (e->ev_join2) cudaEventDestroy(e->ev_join2);
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
   for (auto& m : e->marks)
     if (m) cudaEventDestroy(m);

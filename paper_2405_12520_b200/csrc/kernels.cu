@@ -1267,14 +1267,20 @@ __device__ void replay_finish(const Ctx& c, const Replay& R) {
   for (int32_t q = 0; q < R.nmoved; q++) c.rs_reverted[R.moved[q]] = 0;
 }
 
-// In-place exclusive scan of a[0, n) in shared memory, n <= 2 * blockDim.x;
-// returns the total.  Every thread of the block calls.
-__device__ int32_t block_excl_scan2(int32_t* a, int n) {
+// In-place exclusive scan of a[0, n) (shared or global memory), n <= K *
+// blockDim.x; returns the total.  Every thread of the block calls.
+template <int K>
+__device__ int32_t block_excl_scan(int32_t* a, int n) {
   __shared__ int32_t ws[32];
   const int t = threadIdx.x, lid = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
-  const int i0 = 2 * t, i1 = 2 * t + 1;
-  const int32_t x0 = i0 < n ? a[i0] : 0, x1 = i1 < n ? a[i1] : 0;
-  const int32_t sum = x0 + x1;
+  int32_t x[K];
+  int32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const int i = K * t + k;
+    x[k] = i < n ? a[i] : 0;
+    sum += x[k];
+  }
   int32_t incl = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1293,13 +1299,18 @@ __device__ int32_t block_excl_scan2(int32_t* a, int n) {
     ws[lid] = v;
   }
   __syncthreads();
-  const int32_t base = (w ? ws[w - 1] : 0) + incl - sum;
-  if (i0 < n) a[i0] = base;
-  if (i1 < n) a[i1] = base + x0;
+  int32_t run = (w ? ws[w - 1] : 0) + incl - sum;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    const int i = K * t + k;
+    if (i < n) a[i] = run;
+    run += x[k];
+  }
   const int32_t total = ws[nw - 1];
   __syncthreads();
   return total;
 }
+__device__ __forceinline__ int32_t block_excl_scan2(int32_t* a, int n) { return block_excl_scan<2>(a, n); }
 
 // Closure of the event lanes under "entered member -> its snapshot lane",
 // split into components (one CTA).  Output: dy->n_comp components, comp_off
@@ -1836,15 +1847,10 @@ __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
     }
   }
   __syncthreads();
-  // exclusive prefix of deltas (serial per chunk is fine: nd <= 4096)
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int i = 0; i < nd; i++) {
-      c.patch_prefix[i] = run;
-      run += sd[i];
-    }
-    c.patch_prefix[nd] = run;
-  }
+  // exclusive prefix of the count deltas in lane order
+  const int32_t tot = block_excl_scan<PATCH_MAX / 1024>(sd, nd);
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) c.patch_prefix[i] = sd[i];
+  if (threadIdx.x == 0) c.patch_prefix[nd] = tot;
   (void)warp_sum;
 }
 
@@ -1890,38 +1896,71 @@ __global__ void k_patch_copy(Ctx c) {
 }
 
 // Dirty lanes: gather members, sort (s desc, id asc), write.  Warp per lane.
-__global__ void k_patch_dirty(Ctx c) {
+// Dirty lanes: gather members on chip, sort (s desc, id asc), write.  Warp
+// per lane; lanes with more than PD_CAP members rank straight from global.
+static constexpr int PD_CAP = 128;
+static constexpr int PD_WARPS = 4;
+__global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
   Dyn* dy = c.dyn;
   if (!dy->need_regroup || dy->full_regroup) return;
+  __shared__ VRec sm[PD_WARPS][PD_CAP];
   const VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
   VRec* A = c.lay[dy->cur];
   const int32_t* AS = c.start[dy->cur];
   const int nd = dy->n_dirty;
-  const int lane_id = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   for (int i = gtid() >> 5; i < nd; i += gstride() >> 5) {
     const int32_t L = c.patch_lanes[i];
     const int32_t base = AS[L];
     const int32_t n = c.patch_count[i];
-    // pass 1: collect member indices into the destination range's vix slots
-    // (rank computed against all members; members are few)
-    int pos = 0;
-    for_members(c, C, CS, L, [&](int32_t j) {
-      const VRec r = C[j];
-      int rank = 0;
-      // count members ahead of r
-      for (int32_t q = CS[L]; q < CS[L + 1]; q++)
-        if (C[q].lane == L && ahead_of(C[q].s, C[q].vix, r.s, r.vix)) rank++;
-      for (int32_t q = 0; q < dy->n_moved; q++) {
-        const int32_t jj = c.rs_moved[q];
-        if (C[jj].lane == L && (jj < CS[L] || jj >= CS[L + 1]) && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix)) rank++;
+    if (n <= PD_CAP) {
+      // gather: segment entries still on L, reverted into L, injected into L
+      VRec* m = sm[w];
+      int k = 0;
+      auto take = [&](bool mine, int32_t j) {
+        const unsigned bb = __ballot_sync(0xffffffffu, mine);
+        if (mine) m[k + __popc(bb & ((1u << lane_id) - 1))] = C[j];
+        k += __popc(bb);
+      };
+      for (int32_t b0 = CS[L]; b0 < CS[L + 1]; b0 += 32) {
+        const int32_t j = b0 + lane_id;
+        take(j < CS[L + 1] && C[j].lane == L, j);
       }
-      for (int32_t jj = dy->n_c; jj < dy->n_c + dy->n_inj; jj++)
-        if (C[jj].lane == L && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix)) rank++;
-      if (rank < n) A[base + rank] = r;
-      pos++;
-    });
-    (void)pos;
+      for (int32_t b0 = 0; b0 < dy->n_moved; b0 += 32) {
+        const int32_t q = b0 + lane_id;
+        const int32_t j = q < dy->n_moved ? c.rs_moved[q] : 0;
+        take(q < dy->n_moved && C[j].lane == L && (j < CS[L] || j >= CS[L + 1]), j);
+      }
+      for (int32_t b0 = dy->n_c; b0 < dy->n_c + dy->n_inj; b0 += 32) {
+        const int32_t j = b0 + lane_id;
+        take(j < dy->n_c + dy->n_inj && C[j].lane == L, j);
+      }
+      __syncwarp();
+      for (int a = lane_id; a < n; a += 32) {
+        const double sa = m[a].s;
+        const int32_t va = m[a].vix;
+        int rank = 0;
+        for (int b2 = 0; b2 < n; b2++) rank += ahead_of(m[b2].s, m[b2].vix, sa, va) ? 1 : 0;
+        A[base + rank] = m[a];
+      }
+      __syncwarp();
+    } else {
+      for_members(c, C, CS, L, [&](int32_t j) {
+        const VRec r = C[j];
+        int rank = 0;
+        for (int32_t q = CS[L]; q < CS[L + 1]; q++)
+          if (C[q].lane == L && ahead_of(C[q].s, C[q].vix, r.s, r.vix)) rank++;
+        for (int32_t q = 0; q < dy->n_moved; q++) {
+          const int32_t jj = c.rs_moved[q];
+          if (C[jj].lane == L && (jj < CS[L] || jj >= CS[L + 1]) && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix))
+            rank++;
+        }
+        for (int32_t jj = dy->n_c; jj < dy->n_c + dy->n_inj; jj++)
+          if (C[jj].lane == L && ahead_of(C[jj].s, C[jj].vix, r.s, r.vix)) rank++;
+        if (rank < n) A[base + rank] = r;
+      });
+    }
   }
 }
 
