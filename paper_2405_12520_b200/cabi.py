@@ -137,7 +137,7 @@ def pack_shard(plan) -> Packed:
     return Packed(s, keep)
 
 
-def pack_params(cfg, seed: int, pow_mode: int = 0) -> TsbParams:
+def pack_params(cfg, seed: int, pow_mode: int = 1) -> TsbParams:
     return TsbParams(
         dt=cfg.dt, lookahead=cfg.lookahead,
         idm_v0=cfg.idm.v0, idm_T=cfg.idm.T, idm_a_max=cfg.idm.a_max, idm_b=cfg.idm.b,

@@ -99,3 +99,46 @@ def test_dense_two_lane_reverts():
     assert reverts > 50
     print("reverts", reverts, "sequential-resolve steps", g._report.resolve_sequential)
     _close(g, r)
+
+
+@pytest.mark.parametrize("pow_mode", [1, 0])
+def test_long_queues_oversized_lanes(pow_mode):
+    """1.2 km single-lane blocks under heavy demand: lanes with ~160 vehicles
+    exercise the off-chip paths of k_lanefix (> 64 members) and k_patch_dirty
+    (> 128)."""
+    net = generate_grid(3, 3, block_length=1200.0)
+    trips = random_trips(net, 6000, seed=8, window=(0.0, 150.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 8, 500, every=5, pow_mode=pow_mode)
+    assert int(np.diff(g._state()["lane_start"]).max()) > 128
+    _close(g, r)
+
+
+def test_long_multilane_queues():
+    net = generate_grid(3, 3, block_length=1000.0, lanes_per_direction=2)
+    trips = random_trips(net, 8000, seed=8, window=(0.0, 200.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 8, 500, every=5)
+    _close(g, r)
+
+
+def _star(arms=6, arm=400.0):
+    import math
+    from paper_2405_12520_b200 import BuildOptions, RawJunction, RawRoad, build_network
+    roads = []
+    for k in range(arms):
+        ang = 2 * math.pi * k / arms
+        tip = (arm * math.cos(ang), arm * math.sin(ang))
+        roads.append(RawRoad(f"a{k}_in", [tip, (0.0, 0.0)], 1, 13.9))
+        roads.append(RawRoad(f"a{k}_out", [(0.0, 0.0), tip], 1, 13.9))
+    j = RawJunction("c", [f"a{k}_in" for k in range(arms)], [f"a{k}_out" for k in range(arms)], (0.0, 0.0))
+    return build_network(roads, [j], BuildOptions(coordinate_frame="local", allow_uturns=True))
+
+
+def test_star_junction_many_successors():
+    """A 6-arm junction with U-turns: lanes with 6 successor connectors use the
+    CSR tail of the 4-wide successor table (conn_from_id)."""
+    net = _star()
+    assert max(len(l.successors) for l in net.lanes.values()) > 4
+    trips = random_trips(net, 600, seed=2, window=(0.0, 300.0))
+    g, r, _ = run_pair(net, trips, EngineConfig(), 2, 500, every=5)
+    assert len(g.finished) > 50
+    _close(g, r)
