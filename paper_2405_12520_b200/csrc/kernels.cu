@@ -312,14 +312,18 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         bool have = false;
         double best_inc = 0.0, best_s = 0.0;
         int32_t best_nb = -1;
-        for (int k = 0; k < nsides; k++) {
-          const int32_t nb = sides[k];
-          if (nb < 0) continue;
-          if (!(c.lflag[nb] & LF_OPEN)) continue;
-          const LaneRec LN = c.lanes[nb];
-          if (!mandatory && !any && conn_from_id(c, nb, next_road) < 0) continue;
+        // both sides evaluated without branches (a side that does not exist
+        // or fails a check is evaluated on safe stand-ins and discarded):
+        // the warp stays converged through the fp64 work
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+          const int32_t nb = k < nsides ? sides[k] : -1;
+          const int32_t nbs = nb >= 0 ? nb : snap_lane;
+          bool ok = nb >= 0 && (c.lflag[nbs] & LF_OPEN);
+          const LaneRec LN = c.lanes[nbs];
+          ok = ok && (mandatory || any || conn_from_id(c, nbs, next_road) >= 0);
           const double s_t = me.s * (LN.len / L0.len);
-          const int2 sgn = seg(c, S, nb);
+          const int2 sgn = seg(c, S, nbs);
           const int32_t lo = sgn.x, hi = sgn.y;
           const int32_t m = count_above(A, lo, hi, s_t);
           const int32_t tl_i = m > 0 ? lo + m - 1 : -1;
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           const double g_tl = gap_to(tl, s_t, Lv);
           const double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
           const double g_nf_old = gap_to(tl, tf.s, Lv);
-          if (g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0)) continue;
+          ok = ok && !(g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0));
           const double v0e_tgt = py_min(p.v0, LN.cap);
           const double fr_me_t = (v0e_tgt == v0e_cur) ? fr_me : idm_free<G>(p, v, v0e_tgt);
           const double fr_tf = idm_free<G>(p, tf.v, v0e_tgt);
@@ -337,14 +341,14 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           const double a_nf_new_x = idm_safe<G>(p, fr_tf, tf.v, tf.v - v, g_tf);  // new leader: me at s_t
           const double a_nf = tf.ok ? a_nf_x : 0.0;
           const double a_nf_new = tf.ok ? a_nf_new_x : 0.0;
-          if (tf.ok && a_nf_new < -p.b_safe) continue;
+          ok = ok && !(tf.ok && a_nf_new < -p.b_safe);
           double inc;
           if (a_me == -CUDART_INF)
             inc = CUDART_INF;
           else
             inc = (a_me_new - a_me) + p.politeness * ((a_nf_new - a_nf) + (a_of_new - a_of));
-          if (!mandatory && inc <= p.threshold) continue;
-          if (!have || inc > best_inc || (inc == best_inc && nb < best_nb)) {
+          ok = ok && (mandatory || !(inc <= p.threshold));
+          if (ok && (!have || inc > best_inc || (inc == best_inc && nb < best_nb))) {
             have = true;
             best_inc = inc;
             best_nb = nb;
