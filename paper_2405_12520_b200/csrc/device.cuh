@@ -214,6 +214,7 @@ struct Ctx {
   int32_t* comp_fill;
   int32_t* comp_ev;
   int32_t* dirty_flag;
+  int32_t* cdelta;  // per lane: membership change this step (reverts, injections)
   int32_t* dirty_list;
   int32_t* patch_lanes;
   int32_t* patch_count;

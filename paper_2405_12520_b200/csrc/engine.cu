@@ -898,6 +898,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.comp_fill, 2048));
   RC(dalloc(E, &c.comp_ev, 2048));
   RC(dalloc(E, &c.dirty_flag, NL));
+  RC(dalloc(E, &c.cdelta, NL));
   RC(dalloc(E, &c.dirty_list, NL));
   RC(dalloc(E, &c.patch_lanes, 4096));
   RC(dalloc(E, &c.patch_count, 4096));

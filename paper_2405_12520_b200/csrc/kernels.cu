@@ -1228,6 +1228,8 @@ __device__ void replay(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, 
       c.rs_reverted[rev] = 1;
       R.moved[R.nmoved++] = rev;
       c.rs_movedin[Lb] = 1;
+      atomicAdd(&c.cdelta[L], -1);  // membership change for the regroup
+      atomicAdd(&c.cdelta[Lb], 1);
       if (!c.rs_touched[Lb]) {
         c.rs_touched[Lb] = 1;
         R.touched[R.nt++] = Lb;
@@ -1761,6 +1763,7 @@ __global__ void k_inject_lanes(Ctx c) {
           VRec nr_{o_s, 0.0, vx, (int32_t)cd.route_off, L, -1};
           C[dy->n_c + k] = nr_;
           c.status[vx] = TSB_STATUS_DRIVING;
+          atomicAdd(&c.cdelta[L], 1);
           mark_dirty(c, L);
         }
       }
@@ -1838,17 +1841,13 @@ __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
     c.patch_lanes[r] = x;
   }
   __syncthreads();
-  // new member count of each dirty lane (warp per lane)
-  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  for (int i = w; i < nd; i += blockDim.x >> 5) {
+  // new member count of each dirty lane: its C segment plus the membership
+  // deltas the revert replay and the injection recorded (cdelta)
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
     const int32_t L = c.patch_lanes[i];
-    int cnt = 0;
-    for_members(c, C, CS, L, [&](int32_t) { cnt++; });
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane_id == 0) {
-      c.patch_count[i] = cnt;
-      sd[i] = cnt - (CS[L + 1] - CS[L]);
-    }
+    const int32_t d = c.cdelta[L];
+    c.patch_count[i] = (CS[L + 1] - CS[L]) + d;
+    sd[i] = d;
   }
   __syncthreads();
   // exclusive prefix of the count deltas in lane order
@@ -1972,8 +1971,11 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
 // lane-sorted) becomes the snapshot by swapping the layout buffers.
 __global__ void k_patch_finish(Ctx c) {
   Dyn* dy = c.dyn;
-  // clear dirty flags for the next step
-  for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) c.dirty_flag[c.dirty_list[i]] = 0;
+  // clear dirty flags and membership deltas for the next step
+  for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) {
+    c.dirty_flag[c.dirty_list[i]] = 0;
+    c.cdelta[c.dirty_list[i]] = 0;
+  }
   if (threadIdx.x == 0) {
     if (!dy->need_regroup) {
       dy->cur ^= 1;
