@@ -174,6 +174,8 @@ struct Ctx {
   int32_t* ent;      // per lane: movers entering it this step
   int32_t* mslot;    // per B record (movers): slot among the new lane's entrants
   uint8_t* stay;     // per B record: still on its snapshot lane
+  int2* nrc[2];      // per B record, by step parity: {rptr, next road} of its post-update state
+  int32_t cap_rec;   // capacity of the record layouts
   int32_t* fix_flag;
   int32_t* fix_list;
   unsigned long long* scan_status;   // SCAN_SITES regions of scan_tiles_cap words

@@ -882,6 +882,11 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.ent, NL));
   RC(dalloc(E, &c.mslot, CAP));
   RC(dalloc(E, &c.stay, CAP));
+  for (int b = 0; b < 2; b++) {
+    RC(dalloc(E, &c.nrc[b], CAP));
+    CK(cudaMemset(c.nrc[b], 0xff, sizeof(int2) * CAP));  // rptr -1: no entry
+  }
+  c.cap_rec = (int32_t)CAP;
   RC(dalloc(E, &c.fix_flag, NL));
   RC(dalloc(E, &c.fix_list, NL));
   c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, CAP) / SCAN_TILE + 2);

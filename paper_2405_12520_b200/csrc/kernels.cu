@@ -230,6 +230,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   const uint64_t step_no = (uint64_t)dy->step_no;
   const double new_time = dy->time + p.dt;
   const double Lv = p.L;
+  const int2* nrc_prev = c.nrc[(step_no + 1) & 1];
+  int2* nrc_cur = c.nrc[step_no & 1];
   for (int32_t i = gtid(); i < n; i += gstride()) {
     const VRec me = A[i];
     const int32_t snap_lane = me.lane;
@@ -248,7 +250,18 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     const int2 sg0 = seg(c, S, snap_lane);
     const int32_t lo0 = sg0.x, hi0 = sg0.y;
     const int32_t* roads = c.routes + me.rptr;  // roads[0] = current road, roads[1] = next (or -1)
-    const int32_t next_road = __ldg(roads + 1);
+    // next road of the route: cached by the previous step's update for the
+    // record this snapshot entry came from (src = its index in that step's B,
+    // nearly sequential), so the random route-pool gather leaves the
+    // critical path; the cache entry is keyed by rptr and re-gathered on a
+    // mismatch (reverted, injected, rerouted, ghost records)
+    int32_t next_road;
+    {
+      const int32_t sidx = me.src;
+      int2 ce = make_int2(-1, 0);
+      if (!ghost && sidx >= 0 && sidx < c.cap_rec) ce = __ldg(nrc_prev + sidx);
+      next_road = ce.x == me.rptr ? ce.y : __ldg(roads + 1);
+    }
     const double v = me.v;
     const double v0e_cur = py_min(p.v0, L0.cap);
 
@@ -434,7 +447,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         while (dist < p.lookahead) {
           int32_t nxt;
           if (LC.kind == TSB_KIND_ROAD) {
-            const int32_t nr = __ldg(rq + 1);
+            const int32_t nr = rq == roads ? next_road : __ldg(rq + 1);
             nxt = nr < 0 ? -1 : conn_from_id(c, cur, nr);
             if (nxt < 0 || !(c.lflag[nxt] & LF_OPEN)) break;
           } else {
@@ -477,14 +490,14 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       if (disp < 0.0) disp = 0.0;
     }
     double ns = s + disp, nv = v_new;
-    int32_t nl = lane, nptr = me.rptr;
+    int32_t nl = lane, nptr = me.rptr, nxt_rd = next_road;
 
     // ---- _apply_deltas transitions (world.py:443-499)
     LaneRec LT = L1;
     bool arrived = false, host = false;
     while (ns > LT.len) {
       if (LT.kind == TSB_KIND_ROAD) {
-        const int32_t nr = __ldg(c.routes + nptr + 1);
+        const int32_t nr = nxt_rd;
         if (nr < 0) {
           arrived = true;
           break;
@@ -507,10 +520,12 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         ns -= LT.len;
         nl = LT.succ1;
         nptr += 1;
+        nxt_rd = __ldg(c.routes + nptr + 1);
         LT = c.lanes[nl];
       }
     }
     VRec out{ns, nv, me.vix, nptr, nl, i};
+    nrc_cur[i] = make_int2(nptr, nxt_rd);
     if (arrived && ghost) {  // the owner records it
       out.lane = -1;
       c.stay[i] = 0;
