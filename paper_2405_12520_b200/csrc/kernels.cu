@@ -247,8 +247,13 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       ghost = i >= n_a;
     }
     const LaneRec L0 = c.lanes[snap_lane];
-    const int2 sg0 = seg(c, S, snap_lane);
-    const int32_t lo0 = sg0.x, hi0 = sg0.y;
+    // own-lane neighbours: the adjacent snapshot records, if on the same lane
+    // (a lane's records are contiguous; no CSR lookup on the critical path)
+    // (sharded: ghosts and own records are separate runs of the buffer)
+    const int32_t run_lo = ghost ? n_a : 0, run_hi = ghost ? n : n_a;
+    const VRec prv = i > run_lo ? A[i - 1] : VRec{0.0, 0.0, 0, 0, -1, 0};
+    const VRec nxv = i + 1 < run_hi ? A[i + 1] : VRec{0.0, 0.0, 0, 0, -1, 0};
+    const bool has_prev = prv.lane == snap_lane, has_next = nxv.lane == snap_lane;
     const int32_t* roads = c.routes + me.rptr;  // roads[0] = current road, roads[1] = next (or -1)
     // next road of the route: cached by the previous step's update for the
     // record this snapshot entry came from (src = its index in that step's B,
@@ -307,8 +312,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         // side's three calls are evaluated together: independent fp64
         // chains the scheduler can overlap instead of one long chain.
         const View mev{true, me.s, v};
-        const View cl = view_at(A, i > lo0 ? i - 1 : -1);
-        const View cf = view_at(A, i + 1 < hi0 ? i + 1 : -1);
+        const View cl = has_prev ? View{true, prv.s, prv.v} : View{false, 0.0, 0.0};
+        const View cf = has_next ? View{true, nxv.s, nxv.v} : View{false, 0.0, 0.0};
         const double g_cur = gap_to(cl, me.s, Lv);
         const double g_of_old = me.s - Lv - cf.s;
         const double g_of_new = gap_to(cl, cf.s, Lv);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       if (hi > lo) {
         int32_t ld = -1;
         if (!changed) {
-          if (i > lo0) ld = i - 1;
+          if (has_prev) ld = i - 1;
         } else {
           int32_t m = count_ahead(A, lo, hi, s, me.vix);
           if (m > 0) ld = lo + m - 1;
