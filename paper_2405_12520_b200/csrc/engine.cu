@@ -148,11 +148,28 @@ struct Launcher {
 
 // Kernels go to e->cur: the engine stream, or while a conditional section is
 // being captured, the stream capturing its body graph.
-#define LAUNCH(kc, kern, grid, block, ...)                \
-  do {                                                    \
-    L.pre(kc);                                            \
-    kern<<<(grid), (block), 0, e->cur>>>(__VA_ARGS__);   \
-    L.post();                                             \
+// Launched with programmatic stream serialization (PDL, see kernels.cu
+// PDL_WAIT): the next kernel's launch overlaps the previous kernel's tail.
+template <class... KArgs, class... Args>
+static void launch_pdl(cudaStream_t st, dim3 grid, dim3 block, void (*kern)(KArgs...), Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define LAUNCH(kc, kern, grid, block, ...)                          \
+  do {                                                              \
+    L.pre(kc);                                                      \
+    launch_pdl(e->cur, dim3(grid), dim3(block), kern, __VA_ARGS__); \
+    L.post();                                                       \
   } while (0)
 
 static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in, int32_t* out, int out_sel,

@@ -30,6 +30,12 @@ enum : uint8_t { OUT_NONE = 0, OUT_INJECT = 1, OUT_RETRY = 2, OUT_DROP = 3 };
 
 static constexpr double EPS_GAP = 1e-6;  // world.py:43
 
+// Programmatic dependent launch: kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's launch and
+// prologue overlap the previous kernel's tail; this waits for the previous
+// grid (and its memory) before anything is read.  No-op without the attribute.
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
 
@@ -135,6 +141,7 @@ __device__ __forceinline__ void write_conn_flags(const Ctx& c, int32_t j, const 
 
 // All junctions (after construction and after any host control change).
 __global__ void k_lane_flags(Ctx c) {
+  PDL_WAIT();
   for (int32_t j = gtid(); j < c.n_junc; j += gstride()) write_conn_flags(c, j, c.sig[j]);
 }
 
@@ -221,6 +228,7 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #endif
 template <bool G>
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t n_a = dy->n_a;
   const int32_t n = n_a + (c.sharded ? dy->n_g : 0);
@@ -563,6 +571,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
 
 // Fix-up after host continuation of rerouted vehicles: count their lanes.
 __global__ void k_count_hostq(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const VRec* A = c.lay[dy->cur];
   for (int32_t k = gtid(); k < dy->n_hostq; k += gstride()) {
@@ -590,6 +599,7 @@ template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in, int32_t* out, int out_sel,
                                              const int32_t* n_dev, int32_t n_static, int32_t ntiles,
                                              const int32_t* gate) {
+  PDL_WAIT();
   if (gated_off(gate)) return;
   if (out_sel != SEL_NONE) out = start_buf(c, out_sel);
   unsigned long long* status = c.scan_status + (size_t)site * c.scan_tiles_cap;
@@ -680,6 +690,7 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
 // (arrivals) are dropped.  src has *n_ptr (+ *n_extra) records.
 __global__ void k_scatter(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* n_extra, int start_sel,
                           const int32_t* gate) {
+  PDL_WAIT();
   if (gated_off(gate)) return;
   if (src_sel == SEL_B && gtid() == 0) {
     // vehicles bucketed into C this step (last CSR entry of the scan)
@@ -699,6 +710,7 @@ __global__ void k_scatter(Ctx c, int src_sel, const int32_t* n_ptr, const int32_
 }
 
 __global__ void k_hist(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* n_extra, const int32_t* gate) {
+  PDL_WAIT();
   if (gated_off(gate)) return;
   const VRec* src = rec_buf(c, src_sel);
   const int32_t n = *n_ptr + (n_extra ? *n_extra : 0);
@@ -714,6 +726,7 @@ __global__ void k_hist(Ctx c, int src_sel, const int32_t* n_ptr, const int32_t* 
 // unswept (C keeps the sorted post-delta values) and queued for k_resolve.
 template <bool SWEEP>
 __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
+  PDL_WAIT();
   if (gated_off(gate)) return;
   const VRec* D = c.D;
   VRec* C = rec_buf(c, dst_sel);
@@ -826,6 +839,7 @@ __device__ __forceinline__ void flag_lane(const Ctx& c, int32_t L) {
 }
 
 __global__ void k_place(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
@@ -898,6 +912,7 @@ __global__ void k_place(Ctx c) {
 static constexpr int LX_CAP = 64;   // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
+  PDL_WAIT();
   __shared__ VRec s_in[LX_WARPS][LX_CAP];
   __shared__ VRec s_out[LX_WARPS][LX_CAP];
   Dyn* dy = c.dyn;
@@ -1343,6 +1358,7 @@ __device__ __forceinline__ int32_t block_excl_scan2(int32_t* a, int n) { return 
 // / comp_ev (event lanes per component), comp_size; or dy->complex = 1 when
 // a budget is exceeded (then the sequential replay runs instead).
 __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   __shared__ int32_t cl[CL_CAP];
   __shared__ int32_t lab[CL_CAP];
@@ -1521,6 +1537,7 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
 // One warp per component: the replay restricted to the component's lanes.
 static constexpr int RC_WARPS = 2;
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t nc = dy->n_comp;
   if (nc == 0 || dy->complex) return;
@@ -1557,6 +1574,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
 // Sequential replay of all events (fallback when the closure exceeds the
 // component budgets, or forced by the debug knob).
 __global__ void __launch_bounds__(32) k_resolve(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t ne = dy->n_events;
   if (ne == 0 || !dy->complex) return;
@@ -1598,6 +1616,7 @@ __global__ void __launch_bounds__(32) k_resolve(Ctx c) {
 
 // Lane occupancy after the sweep (max-pressure input, world.py:634-637).
 __global__ void k_lane_counts(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const VRec* C = c.lay[dy->cur ^ 1];
   const int32_t n = dy->n_c;
@@ -1606,6 +1625,7 @@ __global__ void k_lane_counts(Ctx c) {
 
 // world.py:619-647 (+ time/step increment, world.py:677-678).
 __global__ void k_signals(Ctx c) {
+  PDL_WAIT();
   const Params& p = c.p;
   for (int32_t j = gtid(); j < c.n_junc; j += gstride()) {
     if (!c.junc_signal[j]) continue;
@@ -1656,6 +1676,7 @@ __global__ void k_signals(Ctx c) {
 
 // Connector flag bytes from the new junction states (thread per connector).
 __global__ void k_conn_flags(Ctx c) {
+  PDL_WAIT();
   for (int32_t q = gtid(); q < c.n_conn; q += gstride()) {
     const int32_t cn = c.jc[q], j = c.jc_junc[q];
     uint8_t f = c.lflag[cn] & LF_OPEN;
@@ -1670,6 +1691,7 @@ __global__ void k_conn_flags(Ctx c) {
 
 // Build the due list: retry (in due order) ++ pending with departure <= time.
 __global__ void k_inject_due(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   __shared__ int32_t s_new;
   const int32_t nr = dy->n_retry;
@@ -1701,11 +1723,13 @@ __global__ void k_inject_due(Ctx c) {
 }
 
 __global__ void k_inject_hist(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   for (int32_t k = gtid(); k < dy->n_due; k += gstride()) atomicAdd(&c.inj_cnt[c.cold[c.due[k]].origin_lane], 1);
 }
 
 __global__ void k_inject_scatter(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   for (int32_t k = gtid(); k < dy->n_due; k += gstride()) {
     int32_t o = c.cold[c.due[k]].origin_lane;
@@ -1717,6 +1741,7 @@ __global__ void k_inject_scatter(Ctx c) {
 // One thread per origin lane: candidates in due order, gap tests against the
 // lane's current occupants and the vehicles injected before them.
 __global__ void k_inject_lanes(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (dy->n_due == 0) return;
   const Params& p = c.p;
@@ -1793,11 +1818,13 @@ __global__ void k_inject_lanes(Ctx c) {
 }
 
 __global__ void k_retry_flags(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   for (int32_t k = gtid(); k < dy->n_due; k += gstride()) c.flag_in[k] = c.outcome[k] == OUT_RETRY ? 1 : 0;
 }
 
 __global__ void k_retry_compact(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t n = dy->n_due;
   for (int32_t k = gtid(); k < n; k += gstride()) {
@@ -1807,6 +1834,7 @@ __global__ void k_retry_compact(Ctx c) {
 }
 
 __global__ void k_inject_finish(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (dy->n_due > 0) dy->n_retry = c.flag_scan[dy->n_due];
   dy->injected_now = dy->n_inj;
@@ -1835,6 +1863,7 @@ __device__ void for_members(const Ctx& c, const VRec* C, const int32_t* CS, int3
 // One block: decide patch vs full regroup; sort dirty lanes; new counts and
 // the prefix of count deltas in lane order.
 __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int nd = dy->n_dirty;
   if (!dy->need_regroup) return;
@@ -1891,6 +1920,7 @@ __device__ __forceinline__ int32_t dirty_below(const int32_t* lanes, int nd, int
 
 // new_start[L] = C_start[L] + (sum of count deltas of dirty lanes < L)
 __global__ void k_patch_starts(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (!dy->need_regroup || dy->full_regroup) return;
   const int nd = dy->n_dirty;
@@ -1904,6 +1934,7 @@ __global__ void k_patch_starts(Ctx c) {
 
 // Clean lanes keep their sorted segments, shifted.
 __global__ void k_patch_copy(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (!dy->need_regroup || dy->full_regroup) return;
   const VRec* C = c.lay[dy->cur ^ 1];
@@ -1924,6 +1955,7 @@ __global__ void k_patch_copy(Ctx c) {
 static constexpr int PD_CAP = 128;
 static constexpr int PD_WARPS = 4;
 __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (!dy->need_regroup || dy->full_regroup) return;
   __shared__ VRec sm[PD_WARPS][PD_CAP];
@@ -1990,6 +2022,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
 // End of regroup: the new snapshot's size, or -- if nothing moved -- C (already
 // lane-sorted) becomes the snapshot by swapping the layout buffers.
 __global__ void k_patch_finish(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   // clear dirty flags and membership deltas for the next step
   for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) {
@@ -2026,6 +2059,7 @@ __global__ void k_patch_finish(Ctx c) {
 // which joins it), hiding it behind the update; mode 1 is the flush a query
 // issues between steps.  Both use the same order.
 __global__ void k_speeds(Ctx c, int flush) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   if (!(flush ? dy->speeds_pending : dy->acc_now)) return;
   const VRec* A = c.lay[dy->cur];
@@ -2054,10 +2088,12 @@ __global__ void k_speeds(Ctx c, int flush) {
   }
 }
 
-__global__ void k_speeds_done(Ctx c) { c.dyn->speeds_pending = 0; }
+__global__ void k_speeds_done(Ctx c) {
+  PDL_WAIT(); c.dyn->speeds_pending = 0; }
 
 
 __global__ void k_begin_step(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_a;
   dy->finished_now = 0;
@@ -2078,12 +2114,14 @@ __global__ void k_begin_step(Ctx c) {
 }
 
 __global__ void k_set_na(Ctx c, const int32_t* gate) {
+  PDL_WAIT();
   if (gated_off(gate)) return;
   c.dyn->n_a = c.start[c.dyn->cur][c.n_lanes];
 }
 
 // min_front_gap (world.py:694-704) over the snapshot layout.
 __global__ void k_min_gap(Ctx c, double* out) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const VRec* A = c.lay[dy->cur];
   __shared__ double sm[32];
@@ -2113,6 +2151,7 @@ __device__ __forceinline__ int64_t align32(int64_t x) { return (x + 31) & ~(int6
 
 // Own vehicles in the snapshot (vehicle_updates counts them next step).
 __global__ void k_count_own(Ctx c) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t* S = c.start[dy->cur];
   int32_t mine = 0;
@@ -2124,6 +2163,7 @@ __global__ void k_count_own(Ctx c) {
 }
 
 __global__ void k_exp_count(Ctx c) {
+  PDL_WAIT();
   const int32_t* S = c.start[c.dyn->cur];
   for (int32_t e = gtid(); e < c.n_exp; e += gstride()) {
     const int32_t L = c.exp_lane[e];
@@ -2143,6 +2183,7 @@ __device__ __forceinline__ int64_t exp_base(const Ctx& c, int q) {
 
 // Warp per export entry: header count and records.
 __global__ void k_exp_pack(Ctx c, uint8_t* send) {
+  PDL_WAIT();
   const VRec* A = c.lay[c.dyn->cur];
   const int32_t* S = c.start[c.dyn->cur];
   const int lid = threadIdx.x & 31;
@@ -2164,6 +2205,7 @@ struct SrcBase {
   int64_t b[9];
 };
 __global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
+  PDL_WAIT();
   for (int32_t e = gtid(); e < c.n_imp; e += gstride()) {
     const int q = c.imp_peer[e];
     c.imp_cnt[e] = ((const int32_t*)(recv + sb.b[q]))[e - c.peer_first_imp[q]];
@@ -2173,6 +2215,7 @@ __global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
 // Warp per import entry: ghost range of the lane, records appended after the
 // snapshot's own records.
 __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
+  PDL_WAIT();
   Dyn* dy = c.dyn;
   VRec* A = c.lay[dy->cur];
   const int32_t base = dy->n_a;
