@@ -290,15 +290,27 @@ class World:
 
     # ------------------------------------------------------------ records
 
-    def record_step(self, recorder) -> None:
-        """One VehicleRecord per driving vehicle, sorted by id (world.py:771-782)."""
+    def records_arrays(self) -> dict:
+        """The step's vehicle records as numpy arrays, sorted by id -- the batch
+        form of record_step (world.py:771-782): keys
+        ``t`` (float), ``vix`` (dense index), ``id``, ``lane``, ``s``, ``v``,
+        ``angle_deg`` (geometry.py:45-52)."""
         m = self._state()
         order = np.argsort(m["vix"], kind="stable")
         vix, lane, s, v = m["vix"][order], m["lane"][order], m["s"][order], m["v"][order]
-        ang = record_angles(self._flat, lane, s)
-        t = self.time
         ids = self._ft.ids
-        for i, l, a, b, g in zip(vix.tolist(), lane.tolist(), s.tolist(), v.tolist(), ang.tolist()):
+        dense = len(ids) == 0 or (ids[0] == 0 and ids[-1] == len(ids) - 1)
+        id_arr = vix.astype(np.int64) if dense else np.array([ids[i] for i in vix.tolist()], dtype=object)
+        return {"t": self.time, "vix": vix, "id": id_arr, "lane": lane, "s": s, "v": v,
+                "angle_deg": record_angles(self._flat, lane, s)}
+
+    def record_step(self, recorder) -> None:
+        """One VehicleRecord per driving vehicle, sorted by id (world.py:771-782)."""
+        r = self.records_arrays()
+        t = r["t"]
+        ids = self._ft.ids
+        for i, l, a, b, g in zip(r["vix"].tolist(), r["lane"].tolist(), r["s"].tolist(), r["v"].tolist(),
+                                 r["angle_deg"].tolist()):
             recorder.write(VehicleRecord(t=t, id=ids[i], lane=l, s=a, v=b, angle_deg=g))
 
     # ------------------------------------------------------------ road aggregate
