@@ -143,7 +143,9 @@ int tsb_report_get(tsb_engine* e, tsb_report* out);
 
 /* World.prepare() (world.py:211-242): the per-lane index.  Fills the
  * lane-sorted snapshot (lane asc, s desc, id asc): lane_start[n_lanes+1] and
- * per-vehicle vix/lane/road_pos/s/v arrays of capacity >= n_driving. */
+ * per-vehicle vix/lane/road_pos/s/v arrays of capacity >= n_driving
+ * (n_trips suffices; a sharded engine also lists its halo lanes' ghosts:
+ * capacity 2 * n_trips, filter by the shard's zone). */
 int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* vix,
               int32_t* lane, int32_t* road_pos, double* s, double* v);
 /* Per-vix status (TSB_STATUS_*), finish time, and for finished vehicles the

@@ -117,6 +117,8 @@ struct Dyn {
   int32_t speeds_pending;  // the snapshot's road aggregate is not yet accumulated
   int32_t acc_now;         // this step's k_speeds branch accumulates it
   double acc_time;         // the time of that snapshot
+  int32_t n_drv;    // driving vehicles in the snapshot (n_a minus its stale copies)
+  int32_t tail_n;   // records of the lanes the regroup rebuilt into the snapshot's tail
 };
 
 struct Params {
@@ -184,7 +186,7 @@ struct Ctx {
   // sharded mode (shard.py): per-lane zone flags, ghost ranges, export/import lists
   int32_t sharded;
   const uint8_t* zone;  // ZF_OWN | ZF_HALO, ZF_EXACT
-  int2* ghost_seg;      // per halo lane: [start, end) of its ghosts in the snapshot buffer
+
   int32_t n_exp, n_imp;
   const int32_t* exp_lane;  // export entries (peer-major, ascending lanes)
   const int32_t* exp_peer;
@@ -218,9 +220,8 @@ struct Ctx {
   int32_t* dirty_flag;
   int32_t* cdelta;  // per lane: membership change this step (reverts, injections)
   int32_t* dirty_list;
-  int32_t* patch_lanes;
   int32_t* patch_count;
-  int32_t* patch_prefix;
+  int2* rng[2];         // per layout buffer and lane: [start, end) of the lane's records (see seg())
   // resolve scratch
   int32_t* rs_heap;
   uint8_t* rs_inwork;

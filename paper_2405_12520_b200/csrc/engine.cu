@@ -69,7 +69,8 @@ struct tsb_engine {
   // host copies (authoritative for control changes and host continuation)
   int32_t n_lanes = 0, n_roads = 0, n_junc = 0, n_trips = 0;
   int32_t n_pend = 0;  // trips this engine injects (all, or the shard's own)
-  int64_t cap = 0;     // record capacity of the vehicle layouts (2N when sharded: own + ghosts)
+  int64_t cap = 0;     // record capacity of the vehicle layouts (engine.cu create_impl)
+  int64_t span = 1;    // records the one-pass vehicle grids are sized for
   std::vector<LaneRec> lanes;
   std::vector<int32_t> succ, succ_dst_road;
   std::vector<double> phase_dur;
@@ -217,7 +218,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   Ctx& c = e->c;
   Dyn* dy = c.dyn;
   const int VB = 256;
-  const int vgrid = grid_for(e->cap, VB, 1 << 30);  // one pass (no grid-stride tail)
+  const int vgrid = grid_for(e->span, VB, 1 << 30);  // one pass (no grid-stride tail) in the usual case
   const int wgrid = grid_for((int64_t)e->n_lanes * 32, VB, 148 * 32);
   const int tgrid = grid_for(e->n_lanes, VB, 148 * 16);
   const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
@@ -234,9 +235,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     cudaEventRecord(e->ev_join, e->side);
     cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
     if (c.p.pow_glibc)
-      LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+      LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
     else
-      LAUNCH(KC_UPDATE, k_update<false>, grid_for(e->cap, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+      LAUNCH(KC_UPDATE, k_update<false>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
@@ -292,8 +293,6 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
   LAUNCH(KC_REGROUP, k_patch_prepare, 1, 1024, c);
   cond_begin(e, COND_PATCH);
-  LAUNCH(KC_REGROUP, k_patch_starts, tgrid, VB, c);
-  LAUNCH(KC_REGROUP, k_patch_copy, vgrid, VB, c);
   LAUNCH(KC_REGROUP, k_patch_dirty, 296, 32 * PD_WARPS, c);
   cond_end(e);
   cond_begin(e, COND_FULL);
@@ -636,7 +635,6 @@ static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
   c.rank = sh->rank;
   c.nranks = sh->nranks;
   RC(upload(e, (uint8_t**)&c.zone, sh->zone, NL));
-  RC(dalloc(e, &c.ghost_seg, NL));
   std::vector<int32_t> el, ep, il, ip;
   for (int q = 0; q < sh->nranks; q++) {
     c.peer_first_exp[q] = (int64_t)el.size();
@@ -695,7 +693,11 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   const int32_t NR = e->n_roads = net->n_roads;
   const int32_t NJ = e->n_junc = net->n_junctions;
   const int32_t N = e->n_trips = tr->n;
-  const int64_t CAP = e->cap = sh ? 2 * (int64_t)N : (int64_t)N;
+  // record capacity of a layout buffer: the vehicles (own + ghosts when
+  // sharded) plus the rebuilt copies of the lanes the regroup relocated
+  const int64_t CAP = e->cap = sh ? 3 * (int64_t)N : 2 * (int64_t)N;
+  // one-pass grids cover the usual record count; a longer snapshot strides
+  e->span = (sh ? 2 * (int64_t)N : (int64_t)N) + N / 8 + 1024;
   Ctx& c = e->c;
   c.n_lanes = NL;
   c.n_roads = NR;
@@ -922,9 +924,8 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.dirty_flag, NL));
   RC(dalloc(E, &c.cdelta, NL));
   RC(dalloc(E, &c.dirty_list, NL));
-  RC(dalloc(E, &c.patch_lanes, 4096));
   RC(dalloc(E, &c.patch_count, 4096));
-  RC(dalloc(E, &c.patch_prefix, 4097));
+  for (int b = 0; b < 2; b++) RC(dalloc(E, &c.rng[b], NL));
   RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)CAP + 16));
   RC(dalloc(E, &c.rs_inwork, NL));
   RC(dalloc(E, &c.rs_touched, NL));
@@ -1058,7 +1059,7 @@ static void fill_report(const tsb_engine* e, tsb_report* r) {
   const Dyn& d = *e->dyn_host;
   r->time = d.time;
   r->step_no = d.step_no;
-  r->driving = e->c.sharded ? d.n_own : d.n_a;
+  r->driving = e->c.sharded ? d.n_own : d.n_drv;
   r->waiting = (int64_t)(e->n_pend - d.pend_ptr) + d.n_retry;
   r->finished = d.finished_total;
   r->dropped = d.dropped;
@@ -1090,18 +1091,28 @@ int tsb_state(tsb_engine* e, int32_t* n_driving, int32_t* lane_start, int32_t* v
               double* s, double* v) {
   RC(sync_dyn(e));
   const Dyn& d = *e->dyn_host;
-  const int32_t n = d.n_a;
-  *n_driving = n;
-  if (lane_start) CK(cudaMemcpy(lane_start, e->c.start[d.cur], sizeof(int32_t) * (e->n_lanes + 1), cudaMemcpyDeviceToHost));
-  std::vector<VRec> buf(std::max(n, 1));
-  if (n) CK(cudaMemcpy(buf.data(), e->c.lay[d.cur], sizeof(VRec) * n, cudaMemcpyDeviceToHost));
-  for (int32_t k = 0; k < n; k++) {
-    if (vix) vix[k] = buf[k].vix;
-    if (lane) lane[k] = buf[k].lane;
-    if (road_pos) road_pos[k] = (int32_t)(buf[k].rptr - e->cold[buf[k].vix].route_off);
-    if (s) s[k] = buf[k].s;
-    if (v) v[k] = buf[k].v;
+  const int32_t NL = e->n_lanes;
+  // the snapshot in lane order (lane ranges: kernels.cu seg())
+  std::vector<int2> R(std::max(NL, 1));
+  if (NL) CK(cudaMemcpy(R.data(), e->c.rng[d.cur], sizeof(int2) * NL, cudaMemcpyDeviceToHost));
+  const int32_t n_rec = d.n_a + (e->c.sharded ? d.n_g : 0);  // ghosts follow the snapshot
+  std::vector<VRec> buf(std::max(n_rec, 1));
+  if (n_rec) CK(cudaMemcpy(buf.data(), e->c.lay[d.cur], sizeof(VRec) * n_rec, cudaMemcpyDeviceToHost));
+  int32_t k = 0;
+  for (int32_t L = 0; L < NL; L++) {
+    if (lane_start) lane_start[L] = k;
+    const int32_t a = R[L].x, b = R[L].y;
+    for (int32_t j = a; j < b; j++, k++) {
+      const VRec& r = buf[j];
+      if (vix) vix[k] = r.vix;
+      if (lane) lane[k] = r.lane;
+      if (road_pos) road_pos[k] = (int32_t)(r.rptr - e->cold[r.vix].route_off);
+      if (s) s[k] = r.s;
+      if (v) v[k] = r.v;
+    }
   }
+  if (lane_start) lane_start[NL] = k;
+  *n_driving = k;
   return TSB_OK;
 }
 

@@ -60,12 +60,12 @@ __device__ __forceinline__ bool gated_off(const int32_t* gate) { return gate && 
 // Sharded mode (shard.py): lanes are own, halo (ghost copies imported from
 // their owner after every step) or outside the zone.
 enum : uint8_t { ZF_OWN = 1, ZF_HALO = 2, ZF_EXACT = 4 };
-// Snapshot range [x, y) of lane L: its CSR segment, or for a halo lane its
-// ghost range (ghosts live after the snapshot's own records, same buffer).
-__device__ __forceinline__ int2 seg(const Ctx& c, const int32_t* S, int32_t L) {
-  if (c.sharded && (c.zone[L] & ZF_HALO)) return c.ghost_seg[L];
-  return make_int2(S[L], S[L + 1]);
-}
+// Range [x, y) of lane L's records in a layout buffer, R = c.rng[buffer]:
+// written by the scan that lays the buffer out (the lane's CSR segment), then
+// overridden for the lanes the regroup rebuilt into the buffer's tail and,
+// when sharded, for the halo lanes by the ghost import.  Records of the buffer
+// outside their lane's range are stale copies and are skipped.
+__device__ __forceinline__ int2 seg(const Ctx& c, const int2* R, int32_t L) { return R[L]; }
 
 // Conditional graph nodes (engine.cu issue_step): a section of the step graph
 // runs only when its deciding kernel sets the handle.  The handles default to
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   const int32_t n_a = dy->n_a;
   const int32_t n = n_a + (c.sharded ? dy->n_g : 0);
   const VRec* A = c.lay[dy->cur];
-  const int32_t* S = c.start[dy->cur];
+  const int2* S = c.rng[dy->cur];
   const Params& p = c.p;
   const uint64_t step_no = (uint64_t)dy->step_no;
   const double new_time = dy->time + p.dt;
@@ -243,25 +243,24 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   for (int32_t i = gtid(); i < n; i += gstride()) {
     const VRec me = A[i];
     const int32_t snap_lane = me.lane;
-    bool ghost = false;
-    if (c.sharded) {
-      // records of non-own lanes in the snapshot proper are last step's
-      // local copies (superseded by the imported ghosts): drop them
-      if (i < n_a && !(c.zone[snap_lane] & ZF_OWN)) {
-        c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
-        c.stay[i] = 0;
-        continue;
-      }
-      ghost = i >= n_a;
+    const bool ghost = c.sharded && i >= n_a;
+    // a record outside its lane's snapshot range is a stale copy: a lane the
+    // regroup relocated, or (sharded) last step's local copy of a halo lane,
+    // superseded by the imported ghosts -- drop it
+    // own-lane neighbours: the adjacent records of the lane's range (loaded
+    // unconditionally, beside `me`, off the range lookup's critical path)
+    const VRec prv_ = A[i > 0 ? i - 1 : i];
+    const VRec nxv_ = A[i + 1 < n ? i + 1 : i];
+    const int2 sg0 = seg(c, S, snap_lane);
+    if (i < sg0.x || i >= sg0.y || (c.sharded && !ghost && !(c.zone[snap_lane] & ZF_OWN))) {
+      c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
+      c.stay[i] = 0;
+      continue;
     }
     const LaneRec L0 = c.lanes[snap_lane];
-    // own-lane neighbours: the adjacent snapshot records, if on the same lane
-    // (a lane's records are contiguous; no CSR lookup on the critical path)
-    // (sharded: ghosts and own records are separate runs of the buffer)
-    const int32_t run_lo = ghost ? n_a : 0, run_hi = ghost ? n : n_a;
-    const VRec prv = i > run_lo ? A[i - 1] : VRec{0.0, 0.0, 0, 0, -1, 0};
-    const VRec nxv = i + 1 < run_hi ? A[i + 1] : VRec{0.0, 0.0, 0, 0, -1, 0};
-    const bool has_prev = prv.lane == snap_lane, has_next = nxv.lane == snap_lane;
+    const bool has_prev = i > sg0.x, has_next = i + 1 < sg0.y;
+    const VRec prv = has_prev ? prv_ : VRec{0.0, 0.0, 0, 0, -1, 0};
+    const VRec nxv = has_next ? nxv_ : VRec{0.0, 0.0, 0, 0, -1, 0};
     const int32_t* roads = c.routes + me.rptr;  // roads[0] = current road, roads[1] = next (or -1)
     // next road of the route: cached by the previous step's update for the
     // record this snapshot entry came from (src = its index in that step's B,
@@ -601,7 +600,11 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
                                              const int32_t* gate) {
   PDL_WAIT();
   if (gated_off(gate)) return;
-  if (out_sel != SEL_NONE) out = start_buf(c, out_sel);
+  int2* rng = nullptr;
+  if (out_sel != SEL_NONE) {
+    out = start_buf(c, out_sel);
+    rng = out_sel == SEL_A ? c.rng[c.dyn->cur] : c.rng[c.dyn->cur ^ 1];
+  }
   unsigned long long* status = c.scan_status + (size_t)site * c.scan_tiles_cap;
   const int32_t n = n_dev ? *n_dev : n_static;
   __shared__ int32_t s_tile, s_prefix;
@@ -680,6 +683,7 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
   for (int k = 0; k < IPT; k++) {
     int64_t idx = base + (int64_t)threadIdx.x * IPT + k;
     if (idx <= n) out[idx] = run;
+    if (rng && idx < n) rng[idx] = make_int2(run, run + v[k]);
     run += v[k];
   }
 }
@@ -843,7 +847,7 @@ __global__ void k_place(Ctx c) {
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
-  const int32_t* SA = c.start[dy->cur];
+  const int2* SA = c.rng[dy->cur];
   const Params& p = c.p;
   if (gtid() == 0) {
     // vehicles bucketed into C this step (last CSR entry of the scan)
@@ -1860,11 +1864,14 @@ __device__ void for_members(const Ctx& c, const VRec* C, const int32_t* CS, int3
     if (C[j].lane == L) f(j);
 }
 
-// One block: decide patch vs full regroup; sort dirty lanes; new counts and
-// the prefix of count deltas in lane order.
+// One block.  Decides between no rebuild (C becomes the snapshot as is), the patch (C becomes the snapshot
+// and the dirty lanes are rebuilt into its tail, after n_c + n_inj) and the
+// full regroup; for the patch, each dirty lane's new member count and its
+// tail range (exclusive prefix of the counts).
 __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
+  if (threadIdx.x == 0) dy->tail_n = 0;
   const int nd = dy->n_dirty;
   if (!dy->need_regroup) return;
   if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
@@ -1875,83 +1882,28 @@ __global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
     return;
   }
   if (threadIdx.x == 0) set_cond(c, COND_PATCH, true);
-  __shared__ int32_t sl[PATCH_MAX];
   __shared__ int32_t sd[PATCH_MAX];
-  __shared__ int32_t warp_sum[32];
-  const VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) sl[i] = c.dirty_list[i];
-  __syncthreads();
-  // rank sort of the (distinct) dirty lane ids
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-    const int32_t x = sl[i];
-    int r = 0;
-    for (int q = 0; q < nd; q++) r += sl[q] < x ? 1 : 0;
-    c.patch_lanes[r] = x;
-  }
-  __syncthreads();
   // new member count of each dirty lane: its C segment plus the membership
   // deltas the revert replay and the injection recorded (cdelta)
   for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-    const int32_t L = c.patch_lanes[i];
-    const int32_t d = c.cdelta[L];
-    c.patch_count[i] = (CS[L + 1] - CS[L]) + d;
-    sd[i] = d;
+    const int32_t L = c.dirty_list[i];
+    const int32_t n = (CS[L + 1] - CS[L]) + c.cdelta[L];
+    c.patch_count[i] = n;
+    sd[i] = n;
   }
   __syncthreads();
-  // exclusive prefix of the count deltas in lane order
   const int32_t tot = block_excl_scan<PATCH_MAX / 1024>(sd, nd);
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) c.patch_prefix[i] = sd[i];
-  if (threadIdx.x == 0) c.patch_prefix[nd] = tot;
-  (void)warp_sum;
+  const int32_t base = dy->n_c + dy->n_inj;
+  int2* R = c.rng[dy->cur ^ 1];
+  for (int i = threadIdx.x; i < nd; i += blockDim.x)
+    R[c.dirty_list[i]] = make_int2(base + sd[i], base + sd[i] + c.patch_count[i]);
+  if (threadIdx.x == 0) dy->tail_n = tot;
 }
 
-__device__ __forceinline__ int32_t dirty_below(const int32_t* lanes, int nd, int32_t L) {
-  int a = 0, b = nd;
-  while (a < b) {
-    int m = (a + b) >> 1;
-    if (lanes[m] < L)
-      a = m + 1;
-    else
-      b = m;
-  }
-  return a;
-}
-
-// new_start[L] = C_start[L] + (sum of count deltas of dirty lanes < L)
-__global__ void k_patch_starts(Ctx c) {
-  PDL_WAIT();
-  Dyn* dy = c.dyn;
-  if (!dy->need_regroup || dy->full_regroup) return;
-  const int nd = dy->n_dirty;
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  int32_t* AS = c.start[dy->cur];
-  for (int32_t L = gtid(); L <= c.n_lanes; L += gstride()) {
-    const int k = dirty_below(c.patch_lanes, nd, L);
-    AS[L] = CS[L] + c.patch_prefix[k];
-  }
-}
-
-// Clean lanes keep their sorted segments, shifted.
-__global__ void k_patch_copy(Ctx c) {
-  PDL_WAIT();
-  Dyn* dy = c.dyn;
-  if (!dy->need_regroup || dy->full_regroup) return;
-  const VRec* C = c.lay[dy->cur ^ 1];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  VRec* A = c.lay[dy->cur];
-  const int32_t* AS = c.start[dy->cur];
-  const int32_t n = dy->n_c;
-  for (int32_t j = gtid(); j < n; j += gstride()) {
-    const VRec r = C[j];
-    if (c.dirty_flag[r.lane]) continue;
-    A[AS[r.lane] + (j - CS[r.lane])] = r;
-  }
-}
-
-// Dirty lanes: gather members, sort (s desc, id asc), write.  Warp per lane.
-// Dirty lanes: gather members on chip, sort (s desc, id asc), write.  Warp
-// per lane; lanes with more than PD_CAP members rank straight from global.
+// Dirty lanes: gather members on chip, sort (s desc, id asc), write to the
+// lane's tail range.  Warp per lane; lanes with more than PD_CAP members rank
+// straight from global.
 static constexpr int PD_CAP = 128;
 static constexpr int PD_WARPS = 4;
 __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
@@ -1959,15 +1911,15 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
   Dyn* dy = c.dyn;
   if (!dy->need_regroup || dy->full_regroup) return;
   __shared__ VRec sm[PD_WARPS][PD_CAP];
-  const VRec* C = c.lay[dy->cur ^ 1];
+  // sources: [0, n_c + n_inj) of C; destination: the tail of the same buffer
+  VRec* C = c.lay[dy->cur ^ 1];
+  VRec* A = C;
   const int32_t* CS = c.start[dy->cur ^ 1];
-  VRec* A = c.lay[dy->cur];
-  const int32_t* AS = c.start[dy->cur];
   const int nd = dy->n_dirty;
   const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   for (int i = gtid() >> 5; i < nd; i += gstride() >> 5) {
-    const int32_t L = c.patch_lanes[i];
-    const int32_t base = AS[L];
+    const int32_t L = c.dirty_list[i];
+    const int32_t base = c.rng[dy->cur ^ 1][L].x;
     const int32_t n = c.patch_count[i];
     if (n <= PD_CAP) {
       // gather: segment entries still on L, reverted into L, injected into L
@@ -2019,8 +1971,8 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
   }
 }
 
-// End of regroup: the new snapshot's size, or -- if nothing moved -- C (already
-// lane-sorted) becomes the snapshot by swapping the layout buffers.
+// End of regroup: C becomes the snapshot (swap the layout buffers) unless the
+// full regroup rebuilt A; the snapshot's record count and vehicle count.
 __global__ void k_patch_finish(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
@@ -2032,9 +1984,13 @@ __global__ void k_patch_finish(Ctx c) {
   if (threadIdx.x == 0) {
     if (!dy->need_regroup) {
       dy->cur ^= 1;
-      dy->n_a = dy->n_c;
+      dy->n_a = dy->n_drv = dy->n_c;
     } else if (!dy->full_regroup) {
-      dy->n_a = dy->n_c + dy->n_inj;
+      dy->cur ^= 1;
+      dy->n_drv = dy->n_c + dy->n_inj;
+      dy->n_a = dy->n_drv + dy->tail_n;
+    } else {
+      dy->n_drv = dy->n_a;
     }
     // end of step counters
     dy->finished_total += dy->finished_now;
@@ -2063,7 +2019,7 @@ __global__ void k_speeds(Ctx c, int flush) {
   Dyn* dy = c.dyn;
   if (!(flush ? dy->speeds_pending : dy->acc_now)) return;
   const VRec* A = c.lay[dy->cur];
-  const int32_t* S = c.start[dy->cur];
+  const int2* S = c.rng[dy->cur];
   const int32_t wi = (int32_t)((flush ? dy->time : dy->acc_time) / c.p.speed_window);
   if (wi >= c.n_win) {
     if (gtid() == 0) dy->overflow |= 2;
@@ -2074,16 +2030,20 @@ __global__ void k_speeds(Ctx c, int flush) {
   for (int32_t r = gtid() >> 5; r < c.n_roads; r += warps) {
     const int2 span = c.road_span[r];
     if (c.sharded && !(c.zone[span.x] & ZF_OWN)) continue;  // the owner accumulates it
-    const int32_t j0 = S[span.x], j1 = S[span.y + 1];
-    if (j1 == j0) continue;
     double sum = 0.0;
-    for (int32_t j = j0 + lane_id; j < j1; j += 32) sum += A[j].v;
+    int32_t cnt = 0;
+    for (int32_t L = span.x; L <= span.y; L++) {
+      const int2 sg = seg(c, S, L);
+      for (int32_t j = sg.x + lane_id; j < sg.y; j += 32) sum += A[j].v;
+      cnt += sg.y - sg.x;
+    }
+    if (cnt == 0) continue;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane_id == 0) {
       const size_t cell = (size_t)r * c.n_win + wi;
       c.acc_sum[cell] += sum;
-      c.acc_cnt[cell] += j1 - j0;
+      c.acc_cnt[cell] += cnt;
     }
   }
 }
@@ -2095,7 +2055,7 @@ __global__ void k_speeds_done(Ctx c) {
 __global__ void k_begin_step(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
-  dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_a;
+  dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_drv;
   dy->finished_now = 0;
   dy->n_events = 0;
   dy->complex = 0;
@@ -2126,8 +2086,12 @@ __global__ void k_min_gap(Ctx c, double* out) {
   const VRec* A = c.lay[dy->cur];
   __shared__ double sm[32];
   double best = CUDART_INF;
-  for (int32_t i = threadIdx.x; i + 1 < dy->n_a; i += blockDim.x)
-    if (A[i].lane == A[i + 1].lane) best = py_min(best, A[i].s - c.p.L - A[i + 1].s);
+  const int2* S = c.rng[dy->cur];
+  for (int32_t L = threadIdx.x; L < c.n_lanes; L += blockDim.x) {
+    if (c.sharded && !(c.zone[L] & ZF_OWN)) continue;
+    const int2 sg = seg(c, S, L);
+    for (int32_t i = sg.x; i + 1 < sg.y; i++) best = py_min(best, A[i].s - c.p.L - A[i + 1].s);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = best;
@@ -2153,10 +2117,13 @@ __device__ __forceinline__ int64_t align32(int64_t x) { return (x + 31) & ~(int6
 __global__ void k_count_own(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
-  const int32_t* S = c.start[dy->cur];
+  const int2* S = c.rng[dy->cur];
   int32_t mine = 0;
   for (int32_t L = gtid(); L < c.n_lanes; L += gstride())
-    if (c.zone[L] & ZF_OWN) mine += S[L + 1] - S[L];
+    if (c.zone[L] & ZF_OWN) {
+      const int2 sg = seg(c, S, L);
+      mine += sg.y - sg.x;
+    }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&dy->n_own, mine);
@@ -2164,10 +2131,11 @@ __global__ void k_count_own(Ctx c) {
 
 __global__ void k_exp_count(Ctx c) {
   PDL_WAIT();
-  const int32_t* S = c.start[c.dyn->cur];
+  const int2* S = c.rng[c.dyn->cur];
   for (int32_t e = gtid(); e < c.n_exp; e += gstride()) {
     const int32_t L = c.exp_lane[e];
-    c.exp_cnt[e] = S[L + 1] - S[L];
+    const int2 sg = seg(c, S, L);
+    c.exp_cnt[e] = sg.y - sg.x;
   }
 }
 
@@ -2185,7 +2153,7 @@ __device__ __forceinline__ int64_t exp_base(const Ctx& c, int q) {
 __global__ void k_exp_pack(Ctx c, uint8_t* send) {
   PDL_WAIT();
   const VRec* A = c.lay[c.dyn->cur];
-  const int32_t* S = c.start[c.dyn->cur];
+  const int2* S = c.rng[c.dyn->cur];
   const int lid = threadIdx.x & 31;
   for (int32_t e = gtid() >> 5; e < c.n_exp; e += gstride() >> 5) {
     const int q = c.exp_peer[e];
@@ -2195,7 +2163,8 @@ __global__ void k_exp_pack(Ctx c, uint8_t* send) {
     const int32_t n = c.exp_cnt[e];
     if (lid == 0) ((int32_t*)(send + base))[e - e0] = n;
     VRec* dst = (VRec*)(send + base + align32(4 * (c.peer_first_exp[q + 1] - e0))) + (c.exp_pos[e] - c.exp_pos[e0]);
-    for (int32_t k = lid; k < n; k += 32) dst[k] = A[S[L] + k];
+    const int32_t at = seg(c, S, L).x;
+    for (int32_t k = lid; k < n; k += 32) dst[k] = A[at + k];
   }
 }
 
@@ -2228,7 +2197,7 @@ __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
     const VRec* src = (const VRec*)(recv + sb.b[q] + align32(4 * (c.peer_first_imp[q + 1] - e0))) +
                       (c.imp_pos[e] - c.imp_pos[e0]);
     const int32_t at = base + c.imp_pos[e];
-    if (lid == 0) c.ghost_seg[L] = make_int2(at, at + n);
+    if (lid == 0) c.rng[dy->cur][L] = make_int2(at, at + n);
     for (int32_t k = lid; k < n; k += 32) A[at + k] = src[k];
   }
   if (gtid() == 0) dy->n_g = c.imp_pos[c.n_imp];
