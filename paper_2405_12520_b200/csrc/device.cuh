@@ -129,6 +129,7 @@ struct Params {
   double sqrt_ab2;   // 2.0 * sqrt(a_max * b), evaluated as in idm.py:29
   double inv_ab2;    // 1 / sqrt_ab2 when sqrt_ab2 is a power of two (then x / sqrt_ab2 == x * inv_ab2 exactly)
   int32_t ab2_pow2;
+  double rcp_ab2;    // RN(1 / sqrt_ab2): x / sqrt_ab2 by div_rcp()
   uint64_t rng_h2;   // keyed-RNG fold state after (seed, STREAM_MOBIL): constant for the run
   int32_t controller;
   int32_t delta_int; // delta as an integer power if integral in [1, 64], else 0
@@ -306,6 +307,30 @@ __device__ __forceinline__ double div_pos(double x, double y) {
   return z ? x : q;
 }
 
+// x**4 correctly rounded: pow_int_cr(x, 4) with the loop unrolled (the same
+// operations in the same order, so the same bits).
+__device__ __forceinline__ double pow4_cr(double x) {
+  double h, l;
+  dd_mul(x, 0.0, x, 0.0, h, l);
+  dd_mul(h, l, h, l, h, l);
+  return h + l;
+}
+
+// x / b for a divisor fixed for the run, given y = RN(1/b): q = RN(x*y) is
+// within one ulp of x/b, the residual x - b*q is exact (FMA), and
+// RN(q + r*y) is the correctly rounded quotient (Markstein's theorem) as
+// long as nothing under- or overflows -- x outside [2^-900, 2^900] takes the
+// division (never on the model's data: vdv is a product of speeds); zero
+// keeps its sign.
+__device__ __forceinline__ double div_rcp(double x, double b, double y) {
+  const double q = x * y;
+  const double r = fma(-b, q, x);
+  double out = fma(r, y, q);
+  const int ex = (__double2hiint(x) >> 20) & 0x7ff;
+  if (ex < 1023 - 900 || ex > 1023 + 900) out = x / b;
+  return x == 0.0 ? x : out;
+}
+
 // Free-road term (v / v0_eff)**delta (idm.py:24-25).
 // G: glibc-pow arithmetic (compile-time, so each k_update instantiation only
 // carries the code of its own mode).
@@ -313,6 +338,7 @@ template <bool G>
 __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_eff) {
   const double x = div_pos(v, v0_eff);
   if (G) return glibc_pow::pow(x, p.delta);
+  if (p.delta_int == 4) return pow4_cr(x);  // the default delta (params.py)
   return p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);
 }
 
@@ -325,7 +351,9 @@ template <bool G>
 __device__ __forceinline__ double idm_with_free(const Params& p, double fr, double v, double dv, double gap) {
   const bool free_road = isinf(gap);
   const double vdv = v * dv;
-  const double s_star = p.s0 + py_max(0.0, v * p.T + (p.ab2_pow2 ? vdv * p.inv_ab2 : div_pos(vdv, p.sqrt_ab2)));
+  const double s_star = p.s0 + py_max(0.0, v * p.T + (p.ab2_pow2 ? vdv * p.inv_ab2
+                                                      : p.rcp_ab2 != 0.0 ? div_rcp(vdv, p.sqrt_ab2, p.rcp_ab2)
+                                                                         : div_pos(vdv, p.sqrt_ab2)));
   double g = free_road ? 1.0 : gap;
   asm("mov.b64 %0, %0;" : "+d"(g));
   const double q = div_pos(s_star, g);

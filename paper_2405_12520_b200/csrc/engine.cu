@@ -728,6 +728,9 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
     const double m = std::frexp(P.sqrt_ab2, &ex);
     P.ab2_pow2 = (m == 0.5 && std::isfinite(P.sqrt_ab2)) ? 1 : 0;
     P.inv_ab2 = P.ab2_pow2 ? 1.0 / P.sqrt_ab2 : 0.0;
+    // div_rcp needs a divisor whose reciprocal is a normal number with room
+    // to spare; 0 selects the plain division
+    P.rcp_ab2 = (std::isfinite(P.sqrt_ab2) && P.sqrt_ab2 > 0.0 && std::abs(ex) < 500) ? 1.0 / P.sqrt_ab2 : 0.0;
     auto mix = [](uint64_t z) {
       z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;

@@ -347,7 +347,11 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           bool ok = nb >= 0 && (c.lflag[nbs] & LF_OPEN);
           const LaneRec LN = c.lanes[nbs];
           ok = ok && (mandatory || any || conn_from_id(c, nbs, next_road) >= 0);
-          const double s_t = me.s * (LN.len / L0.len);
+          // lanes of one road share its length: the ratio is then exactly 1
+          // (a branch, so the division is skipped, not just discarded)
+          double ratio = 1.0;
+          if (LN.len != L0.len) ratio = LN.len / L0.len;
+          const double s_t = me.s * ratio;
           const int2 sgn = seg(c, S, nbs);
           const int32_t lo = sgn.x, hi = sgn.y;
           const int32_t m = count_above(A, lo, hi, s_t);
