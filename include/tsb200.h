@@ -198,7 +198,8 @@ int tsb_set_pow_mode(tsb_engine* e, int32_t pow_mode);
 int tsb_mark(tsb_engine* e, int32_t slot);
 int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
 /* Test knobs: bit 0 forces the sequential revert-chain resolver, bit 1 the
- * full (non-incremental) regroup.  Results must not change. */
+ * full (non-incremental) regroup, bit 2 the general (closure + components)
+ * resolver instead of the per-event fast path.  Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);
 /* Kernel launches issued per step (for the bench's gpu_launches claim). */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);

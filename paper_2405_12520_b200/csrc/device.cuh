@@ -119,6 +119,9 @@ struct Dyn {
   double acc_time;         // the time of that snapshot
   int32_t n_drv;    // driving vehicles in the snapshot (n_a minus its stale copies)
   int32_t tail_n;   // records of the lanes the regroup rebuilt into the snapshot's tail
+  int32_t rf_arrive;    // k_resolve_fast: warps past the claim phase
+  int32_t rf_conflict;  // k_resolve_fast: closures overlap or exceed a budget (general path)
+  int32_t rf_done;      // k_resolve_fast replayed every event
 };
 
 struct Params {
@@ -231,6 +234,7 @@ struct Ctx {
   uint8_t* rs_movedin;
   int32_t* rs_moved;
   uint8_t* rs_reverted;
+  unsigned long long* rf_owner;  // per lane: (step epoch << 32) | (event + 1) of the closure that claimed it
   int32_t* rs_members;
   int32_t* rs_touched_list;
   // injection

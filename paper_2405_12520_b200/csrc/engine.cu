@@ -261,8 +261,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     e->cur = main_s;
   }
   // exact revert resolution (only when some lane's sweep reverts)
+  LAUNCH(KC_RESOLVE, k_resolve_fast, RF_BLOCKS, 32 * RC_WARPS, c);
+  cond_begin(e, COND_RESOLVE);  // events whose closures meet or overflow a budget
   LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
-  cond_begin(e, COND_RESOLVE);
   LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
   cond_end(e);
@@ -933,6 +934,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.rs_inwork, NL));
   RC(dalloc(E, &c.rs_touched, NL));
   RC(dalloc(E, &c.rs_event, NL));
+  RC(dalloc(E, &c.rf_owner, NL));
   RC(dalloc(E, &c.rs_movedin, NL));
   RC(dalloc(E, &c.rs_moved, CAP));
   RC(dalloc(E, &c.rs_reverted, CAP));

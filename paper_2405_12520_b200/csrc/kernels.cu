@@ -1373,8 +1373,8 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
   __shared__ int32_t eu[CE_CAP], ev[CE_CAP];
   __shared__ int32_t indeg[CL_CAP];
   __shared__ int32_t s_n, s_ne, s_over, s_changed, s_ncomp;
+  if (dy->rf_done) return;  // k_resolve_fast replayed the events (eager mode runs this section)
   const int32_t ne = dy->n_events;
-  if (threadIdx.x == 0) set_cond(c, COND_RESOLVE, ne > 0);
   // clear the previous step's closure marks
   for (int32_t q = threadIdx.x; q < dy->n_cl; q += blockDim.x) c.cl_idx[c.cl_lanes[q]] = 0;
   __syncthreads();
@@ -1544,11 +1544,131 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
 
 // One warp per component: the replay restricted to the component's lanes.
 static constexpr int RC_WARPS = 2;
+
+// The common case without the closure kernel: every event's closure is
+// computed by its own warp (breadth-first over "entered member -> its
+// snapshot lane", as k_resolve_closure), lanes are claimed in rf_owner
+// (epoch-tagged: no clearing), and if no two closures meet and each fits the
+// component budgets, each event is a component of its own and its warp
+// replays it at once.  Otherwise nothing was modified except the claims and
+// the general path (closure, components, sequential fallback) runs in the
+// COND_RESOLVE section.  The warps of one launch wait for each other once
+// (all co-resident: at most RF_BLOCKS small blocks).
+static constexpr int RF_BLOCKS = 64;
+__global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
+  PDL_WAIT();
+  Dyn* dy = c.dyn;
+  const int32_t ne = dy->n_events;
+  if (ne == 0) return;
+  if (ne > RF_BLOCKS * RC_WARPS || (c.debug & 5)) {  // debug bit 0: sequential, bit 2: general path
+    if (gtid() == 0) set_cond(c, COND_RESOLVE, true);
+    return;
+  }
+  const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
+  const int32_t ev = blockIdx.x * RC_WARPS + w;
+  if (ev >= ne) return;
+  __shared__ RsM sm[RC_WARPS][RS_CAP];
+  __shared__ RsM st[RC_WARPS][RS_CAP];
+  __shared__ int32_t sh[RC_WARPS][HCAP], smv[RC_WARPS][2 * HCAP], stl[RC_WARPS][HCAP];
+  __shared__ int32_t s_bad[RC_WARPS];
+  VRec* C = c.lay[dy->cur ^ 1];
+  const int32_t* CS = c.start[dy->cur ^ 1];
+  const VRec* A = c.lay[dy->cur];
+  const unsigned long long mine = ((unsigned long long)(uint32_t)(dy->step_no + 1) << 32) | (uint32_t)(ev + 1);
+  const unsigned long long epoch = mine >> 32;
+  int32_t* q = stl[w];  // closure lanes (the touched list is filled only later, by the replay)
+  // claim lane T for this closure: 1 new, 0 already ours, -1 another closure's
+  auto claim = [&](int32_t T) -> int {
+    unsigned long long old = c.rf_owner[T];
+    for (;;) {
+      if ((old >> 32) == epoch) return old == mine ? 0 : -1;
+      const unsigned long long got = atomicCAS(c.rf_owner + T, old, mine);
+      if (got == old) return 1;
+      old = got;
+    }
+  };
+  const int32_t E = c.events[ev];
+  int32_t qn = 1, nedge = 0;
+  bool bad = false;
+  if (lid == 0) {
+    q[0] = E;
+    bad = claim(E) < 0;
+  }
+  bad = __shfl_sync(0xffffffffu, (int)bad, 0);
+  for (int32_t h = 0; h < qn && !bad; h++) {
+    const int32_t L = q[h];
+    const int32_t j0 = CS[L], j1 = CS[L + 1];
+    for (int32_t b0 = j0; b0 < j1; b0 += 32) {
+      const int32_t j = b0 + lid;
+      int32_t T = L;
+      if (j < j1) T = A[C[j].src].lane;
+      const bool entered = T != L;
+      const unsigned em = __ballot_sync(0xffffffffu, entered);
+      nedge += __popc(em);
+      // append newly claimed origin lanes, one lane at a time (few per lane)
+      unsigned pend = em;
+      while (pend) {
+        const int src_l = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const int32_t Tk = __shfl_sync(0xffffffffu, T, src_l);
+        int r = 0;
+        if (lid == 0) r = claim(Tk);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (r < 0) bad = true;
+        if (r == 1) {
+          if (qn >= HCAP) {
+            bad = true;
+          } else {
+            if (lid == 0) q[qn] = Tk;
+            qn++;
+          }
+        }
+      }
+    }
+    // on-chip budget: a lane's members plus every edge of the closure (a
+    // bound on the vehicles that can be reverted into it)
+    if (j1 - j0 + nedge > RS_CAP || nedge > 2 * HCAP) bad = true;
+    __syncwarp();
+  }
+  // the budget check above used the edges found so far; recheck with all
+  if (!bad)
+    for (int32_t h = 0; h < qn; h++)
+      if (CS[q[h] + 1] - CS[q[h]] + nedge > RS_CAP) bad = true;
+  if (lid == 0) {
+    if (bad) atomicExch(&dy->rf_conflict, 1);
+    __threadfence();
+    atomicAdd(&dy->rf_arrive, 1);
+    while (atomicAdd(&dy->rf_arrive, 0) < ne) __nanosleep(64);
+    __threadfence();
+    s_bad[w] = atomicAdd(&dy->rf_conflict, 0);
+  }
+  __syncwarp();
+  if (s_bad[w]) {
+    if (ev == 0) set_cond(c, COND_RESOLVE, true);
+    return;
+  }
+  if (ev == 0) dy->rf_done = 1;  // read by the general path's kernels in eager mode
+  Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
+  if (lid == 0) {
+    c.rs_event[E] = 1;
+    c.rs_inwork[E] = 1;
+    heap_push(R.heap, R.hn, E);
+  }
+  __syncwarp();
+  replay(c, C, CS, A, R, sm[w], st[w], (int64_t)dy->n_c + 2);
+  if (lid == 0) {
+    replay_finish(c, R);
+    if (c.sharded && R.zf == 3) dy->overflow |= 16;
+    const int32_t base = atomicAdd(&dy->n_moved, R.nmoved);
+    for (int32_t k = 0; k < R.nmoved; k++) c.rs_moved[base + k] = R.moved[k];
+    atomicAdd((unsigned long long*)&dy->reverts_last, (unsigned long long)R.reverts);
+  }
+}
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t nc = dy->n_comp;
-  if (nc == 0 || dy->complex) return;
+  if (nc == 0 || dy->complex || dy->rf_done) return;
   __shared__ RsM sm[RC_WARPS][RS_CAP];
   __shared__ RsM st[RC_WARPS][RS_CAP];
   __shared__ int32_t sh[RC_WARPS][HCAP], smv[RC_WARPS][2 * HCAP], stl[RC_WARPS][HCAP];
@@ -2075,6 +2195,9 @@ __global__ void k_begin_step(Ctx c) {
   dy->speeds_pending = 0;
   dy->reverts_last = 0;
   dy->n_due = 0;
+  dy->rf_arrive = 0;
+  dy->rf_conflict = 0;
+  dy->rf_done = 0;
 }
 
 __global__ void k_set_na(Ctx c, const int32_t* gate) {

@@ -80,10 +80,11 @@ def test_ring_stop_and_go():
     _close(g, r)
 
 
-@pytest.mark.parametrize("debug", [0, 1, 2, 3])
+@pytest.mark.parametrize("debug", [0, 1, 2, 3, 4, 6])
 def test_dense_short_blocks_revert_chains(debug):
-    """Up to 35 reverts per step: parallel fast path, forced sequential
-    replay (bit 0) and forced full regroup (bit 1) must all match the oracle."""
+    """Up to 35 reverts per step: per-event fast path, forced sequential
+    replay (bit 0), forced full regroup (bit 1) and forced closure/component
+    resolver (bit 2) must all match the oracle."""
     net = generate_grid(6, 6, block_length=60.0)
     trips = random_trips(net, 6000, seed=5, window=(0.0, 200.0))
     g, r, reverts = run_pair(net, trips, EngineConfig(), 5, 400, every=2, debug=debug)
