@@ -249,6 +249,20 @@ def barrier(pg):
         pg.barrier()
 
 
+PATHS = ("resolve_fast", "resolve_general", "regroup_patch", "regroup_full", "inject")
+
+
+def path_counters(L, h):
+    """Cumulative counts of the step paths taken (tsb_path_counters)."""
+    import ctypes as C
+
+    from paper_2405_12520_b200 import _native
+
+    out = (C.c_int64 * len(PATHS))()
+    _native.check(L.tsb_path_counters(h, out))
+    return list(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -259,6 +273,7 @@ def main():
     ap.add_argument("--spacing", type=float, default=29.0)
     ap.add_argument("--cpu-sample-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--debug", type=int, default=0, help="tsb_set_debug flags (experiments; results unchanged)")
     ap.add_argument("--pow", default="correct", choices=["correct", "glibc"],
                     help="IDM power arithmetic of the headline run: correctly rounded (within the "
                          "north-star tolerance of the reference) or glibc pow (bit-identical to the "
@@ -309,13 +324,17 @@ def main():
     world.step()  # bulk injection of all pre-placed vehicles (excluded)
     n_drv = world.driving_count()
     L = _native.lib()
+    if args.debug:
+        _native.check(L.tsb_set_debug(world._h, args.debug))
     hbm, peak_src = load_peaks()
     with ClockSampler(local) as clk:
         world.run(args.warmup)
         barrier(pg)
         u0 = world.vehicle_updates
+        pc0 = path_counters(L, world._h)
         ms = C.c_double()
         _native.check(L.tsb_time_steps(world._h, args.steps, C.byref(ms)))  # CUDA events, engine stream
+        pc1 = path_counters(L, world._h)
         world._report = world._report  # counters refreshed by tsb_time_steps' sync
         r = world._report
         _native.check(L.tsb_report_get(world._h, C.byref(r)))
@@ -392,6 +411,7 @@ def main():
                                    "reference, integer facts identical); glibc = glibc pow restated on the device, "
                                    "record streams byte-identical to the reference (tests/test_gpu_golden.py)"},
                    "reverts_per_step": r_end.reverts_total / max(1, r_end.step_no),
+                   "paths_per_timed_step": {k: (pc1[i] - pc0[i]) / args.steps for i, k in enumerate(PATHS)},
                    "sequential_resolve_steps": r_end.resolve_sequential, "steps_total": r_end.step_no},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": C.sizeof(r),

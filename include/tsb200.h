@@ -199,8 +199,16 @@ int tsb_mark(tsb_engine* e, int32_t slot);
 int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
 /* Test knobs: bit 0 forces the sequential revert-chain resolver, bit 1 the
  * full (non-incremental) regroup, bit 2 the general (closure + components)
- * resolver instead of the per-event fast path.  Results must not change. */
+ * resolver instead of the per-event fast path, bit 3 a step graph without
+ * conditional nodes (every section's kernels launched, gating themselves).
+ * Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);
+/* Which step paths ran so far (measurement hook): out[0] steps whose revert
+ * events were all replayed by the per-event fast path, out[1] steps that
+ * needed the general resolver, out[2] incremental (patch) regroups, out[3]
+ * full regroups, out[4] steps that ran the injection section. */
+#define TSB_PATH_COUNTERS 5
+int tsb_path_counters(tsb_engine* e, int64_t* out);
 /* Kernel launches issued per step (for the bench's gpu_launches claim). */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);
 

@@ -46,6 +46,7 @@ SIGNATURES = {
     "tsb_time_steps": (_i32, [_vp, _i32, C.POINTER(_f64)]),
     "tsb_launches_per_step": (_i32, [_vp, C.POINTER(_i32)]),
     "tsb_set_debug": (_i32, [_vp, _i32]),
+    "tsb_path_counters": (_i32, [_vp, _vp]),
     "tsb_create_sharded": (_i32, [_vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
     "tsb_mark": (_i32, [_vp, _i32]),
     "tsb_set_pow_mode": (_i32, [_vp, _i32]),

@@ -122,6 +122,9 @@ struct Dyn {
   int32_t rf_arrive;    // k_resolve_fast: warps past the claim phase
   int32_t rf_conflict;  // k_resolve_fast: closures overlap or exceed a budget (general path)
   int32_t rf_done;      // k_resolve_fast replayed every event
+  int32_t pad2_;
+  // cumulative step-path counters (tsb_path_counters)
+  int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };
 
 struct Params {

@@ -184,7 +184,7 @@ static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in
 // whose body captures every launch until cond_end.  Outside capture both are
 // no-ops and the section's kernels gate themselves on the same flags.
 static void cond_begin(tsb_engine* e, int k) {
-  if (!e->capturing) return;
+  if (!e->capturing || !e->c.use_cond) return;
   cudaStreamCaptureStatus st;
   unsigned long long id;
   cudaGraph_t g;
@@ -207,7 +207,7 @@ static void cond_begin(tsb_engine* e, int k) {
   e->cur = e->body;
 }
 static void cond_end(tsb_engine* e) {
-  if (!e->capturing) return;
+  if (!e->capturing || !e->c.use_cond) return;
   cudaError_t er = cudaStreamEndCapture(e->body, &e->body_graph);
   if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
   e->cur = e->stream;
@@ -225,7 +225,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   const int cgrid = grid_for(std::max(c.n_conn, 1), VB, 148 * 8);
   const int32_t NL = e->n_lanes;
   if (phase != 2) {
-    LAUNCH(KC_MISC, k_begin_step, 1, 1, c);
+    LAUNCH(KC_MISC, k_begin_step, grid_for(NL, VB, 148 * 4), VB, c);  // + zeroes the lane counts
     // previous step's road aggregate on a parallel branch (joined before the regroup)
     cudaEventRecord(e->ev_fork, e->cur);
     cudaStreamWaitEvent(e->side, e->ev_fork, 0);
@@ -233,7 +233,6 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     k_speeds<<<grid_for((int64_t)std::max(e->n_roads, 1) * 32, VB, 1 << 30), VB, 0, e->side>>>(c, 0);
     L.post();
     cudaEventRecord(e->ev_join, e->side);
-    cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
     if (c.p.pow_glibc)
       LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
     else
@@ -574,11 +573,11 @@ static int build_graph(tsb_engine* e) {
     const cudaGraphNode_t* deps;
     size_t nd;
     CK(cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd));
-    for (int k = 0; k < N_COND; k++)
+    for (int k = 0; k < N_COND && !(e->c.debug & 8); k++)
       CK(cudaGraphConditionalHandleCreate((cudaGraphConditionalHandle*)&e->c.cond[k], g, 0,
                                           cudaGraphCondAssignDefault));
   }
-  e->c.use_cond = 1;
+  e->c.use_cond = (e->c.debug & 8) ? 0 : 1;  // debug bit 3: gated kernels instead of IF nodes
   e->capturing = true;
   e->capture_err = cudaSuccess;
   Launcher L{e};
@@ -1340,6 +1339,15 @@ int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms) {
 int tsb_set_debug(tsb_engine* e, int32_t flags) {
   e->c.debug = flags;
   e->graph_dirty = true;
+  return TSB_OK;
+}
+
+int tsb_path_counters(tsb_engine* e, int64_t* out) {
+  RC(sync_dyn(e));
+  const Dyn& d = *e->dyn_host;
+  const int64_t v[TSB_PATH_COUNTERS] = {d.n_resolve_fast, d.n_resolve_general, d.n_regroup_patch,
+                                        d.n_regroup_full, d.n_inject_steps};
+  for (int k = 0; k < TSB_PATH_COUNTERS; k++) out[k] = v[k];
   return TSB_OK;
 }
 

@@ -1561,7 +1561,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   const int32_t ne = dy->n_events;
   if (ne == 0) return;
   if (ne > RF_BLOCKS * RC_WARPS || (c.debug & 5)) {  // debug bit 0: sequential, bit 2: general path
-    if (gtid() == 0) set_cond(c, COND_RESOLVE, true);
+    if (gtid() == 0) {
+      set_cond(c, COND_RESOLVE, true);
+      dy->n_resolve_general++;
+    }
     return;
   }
   const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
@@ -1587,6 +1590,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
       old = got;
     }
   };
+#ifdef TSB_RF_TRACE
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
   const int32_t E = c.events[ev];
   int32_t qn = 1, nedge = 0;
   bool bad = false;
@@ -1634,6 +1641,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   if (!bad)
     for (int32_t h = 0; h < qn; h++)
       if (CS[q[h] + 1] - CS[q[h]] + nedge > RS_CAP) bad = true;
+#ifdef TSB_RF_TRACE
+  unsigned long long t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+#endif
   if (lid == 0) {
     if (bad) atomicExch(&dy->rf_conflict, 1);
     __threadfence();
@@ -1644,10 +1655,16 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   }
   __syncwarp();
   if (s_bad[w]) {
-    if (ev == 0) set_cond(c, COND_RESOLVE, true);
+    if (ev == 0 && lid == 0) {
+      set_cond(c, COND_RESOLVE, true);
+      dy->n_resolve_general++;
+    }
     return;
   }
-  if (ev == 0) dy->rf_done = 1;  // read by the general path's kernels in eager mode
+  if (ev == 0 && lid == 0) {
+    dy->rf_done = 1;  // read by the general path's kernels in eager mode
+    dy->n_resolve_fast++;
+  }
   Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
   if (lid == 0) {
     c.rs_event[E] = 1;
@@ -1655,7 +1672,18 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     heap_push(R.heap, R.hn, E);
   }
   __syncwarp();
+#ifdef TSB_RF_TRACE
+  unsigned long long t2;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+#endif
   replay(c, C, CS, A, R, sm[w], st[w], (int64_t)dy->n_c + 2);
+#ifdef TSB_RF_TRACE
+  unsigned long long t3;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+  if (lid == 0)
+    printf("RF step %lld ev %d/%d E %d qn %d edges %d lanes_touched %d reverts %lld bfs %llu wait %llu replay %llu ns\n",
+           (long long)dy->step_no, ev, ne, E, qn, nedge, R.nt, (long long)R.reverts, t1 - t0, t2 - t1, t3 - t2);
+#endif
   if (lid == 0) {
     replay_finish(c, R);
     if (c.sharded && R.zf == 3) dy->overflow |= 16;
@@ -1847,6 +1875,7 @@ __global__ void k_inject_due(Ctx c) {
     dy->n_retry = 0;
     dy->injected_now = 0;
     set_cond(c, COND_INJECT, nr + nn > 0);
+    if (nr + nn > 0) dy->n_inject_steps++;
   }
 }
 
@@ -2113,8 +2142,10 @@ __global__ void k_patch_finish(Ctx c) {
       dy->cur ^= 1;
       dy->n_drv = dy->n_c + dy->n_inj;
       dy->n_a = dy->n_drv + dy->tail_n;
+      dy->n_regroup_patch++;
     } else {
       dy->n_drv = dy->n_a;
+      dy->n_regroup_full++;
     }
     // end of step counters
     dy->finished_total += dy->finished_now;
@@ -2178,6 +2209,8 @@ __global__ void k_speeds_done(Ctx c) {
 
 __global__ void k_begin_step(Ctx c) {
   PDL_WAIT();
+  for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) c.cnt[L] = 0;
+  if (gtid() != 0) return;
   Dyn* dy = c.dyn;
   dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_drv;
   dy->finished_now = 0;
