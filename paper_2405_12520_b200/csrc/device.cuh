@@ -122,7 +122,7 @@ struct Dyn {
   int32_t rf_arrive;    // k_resolve_fast: warps past the claim phase
   int32_t rf_conflict;  // k_resolve_fast: closures overlap or exceed a budget (general path)
   int32_t rf_done;      // k_resolve_fast replayed every event
-  int32_t pad2_;
+  int32_t rg_done;      // k_regroup: blocks finished (the last one ends the step)
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };
@@ -227,7 +227,6 @@ struct Ctx {
   int32_t* dirty_flag;
   int32_t* cdelta;  // per lane: membership change this step (reverts, injections)
   int32_t* dirty_list;
-  int32_t* patch_count;
   int2* rng[2];         // per layout buffer and lane: [start, end) of the lane's records (see seg())
   // resolve scratch
   int32_t* rs_heap;

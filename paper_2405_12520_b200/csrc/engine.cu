@@ -291,10 +291,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   // next snapshot: nothing if no lane changed membership/order; else rebuild
   // only the dirty lanes and shift the rest; full regroup if too many changed
   cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
-  LAUNCH(KC_REGROUP, k_patch_prepare, 1, 1024, c);
-  cond_begin(e, COND_PATCH);
-  LAUNCH(KC_REGROUP, k_patch_dirty, 296, 32 * PD_WARPS, c);
-  cond_end(e);
+  LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c);
   cond_begin(e, COND_FULL);
   cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
   LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->full_regroup);
@@ -302,8 +299,8 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
-  cond_end(e);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
+  cond_end(e);
   if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
 }
 
@@ -927,7 +924,6 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.dirty_flag, NL));
   RC(dalloc(E, &c.cdelta, NL));
   RC(dalloc(E, &c.dirty_list, NL));
-  RC(dalloc(E, &c.patch_count, 4096));
   for (int b = 0; b < 2; b++) RC(dalloc(E, &c.rng[b], NL));
   RC(dalloc(E, &c.rs_heap, (size_t)NL + 2 * (size_t)CAP + 16));
   RC(dalloc(E, &c.rs_inwork, NL));

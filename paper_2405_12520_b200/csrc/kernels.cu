@@ -71,7 +71,7 @@ __device__ __forceinline__ int2 seg(const Ctx& c, const int2* R, int32_t L) { re
 // runs only when its deciding kernel sets the handle.  The handles default to
 // 0 at every graph launch; in eager launches (profiling, host-continuation
 // mode) use_cond is 0 and the sections' kernels gate themselves instead.
-enum { COND_RESOLVE = 0, COND_INJECT = 1, COND_PATCH = 2, COND_FULL = 3, N_COND = 4 };
+enum { COND_RESOLVE = 0, COND_INJECT = 1, COND_FULL = 2, N_COND = 3 };
 __device__ __forceinline__ void set_cond(const Ctx& c, int k, bool v) {
   if (c.use_cond && v) cudaGraphSetConditional(c.cond[k], 1u);
 }
@@ -2017,66 +2017,19 @@ __device__ void for_members(const Ctx& c, const VRec* C, const int32_t* CS, int3
     if (C[j].lane == L) f(j);
 }
 
-// One block.  Decides between no rebuild (C becomes the snapshot as is), the patch (C becomes the snapshot
-// and the dirty lanes are rebuilt into its tail, after n_c + n_inj) and the
-// full regroup; for the patch, each dirty lane's new member count and its
-// tail range (exclusive prefix of the counts).
-__global__ void __launch_bounds__(1024) k_patch_prepare(Ctx c) {
-  PDL_WAIT();
-  Dyn* dy = c.dyn;
-  if (threadIdx.x == 0) dy->tail_n = 0;
-  const int nd = dy->n_dirty;
-  if (!dy->need_regroup) return;
-  if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
-    if (threadIdx.x == 0) {
-      dy->full_regroup = 1;
-      set_cond(c, COND_FULL, true);
-    }
-    return;
-  }
-  if (threadIdx.x == 0) set_cond(c, COND_PATCH, true);
-  __shared__ int32_t sd[PATCH_MAX];
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  // new member count of each dirty lane: its C segment plus the membership
-  // deltas the revert replay and the injection recorded (cdelta)
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-    const int32_t L = c.dirty_list[i];
-    const int32_t n = (CS[L + 1] - CS[L]) + c.cdelta[L];
-    c.patch_count[i] = n;
-    sd[i] = n;
-  }
-  __syncthreads();
-  const int32_t tot = block_excl_scan<PATCH_MAX / 1024>(sd, nd);
-  const int32_t base = dy->n_c + dy->n_inj;
-  int2* R = c.rng[dy->cur ^ 1];
-  for (int i = threadIdx.x; i < nd; i += blockDim.x)
-    R[c.dirty_list[i]] = make_int2(base + sd[i], base + sd[i] + c.patch_count[i]);
-  if (threadIdx.x == 0) dy->tail_n = tot;
-}
-
 // Dirty lanes: gather members on chip, sort (s desc, id asc), write to the
 // lane's tail range.  Warp per lane; lanes with more than PD_CAP members rank
 // straight from global.
 static constexpr int PD_CAP = 128;
 static constexpr int PD_WARPS = 4;
-__global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
-  PDL_WAIT();
-  Dyn* dy = c.dyn;
-  if (!dy->need_regroup || dy->full_regroup) return;
-  __shared__ VRec sm[PD_WARPS][PD_CAP];
-  // sources: [0, n_c + n_inj) of C; destination: the tail of the same buffer
-  VRec* C = c.lay[dy->cur ^ 1];
-  VRec* A = C;
-  const int32_t* CS = c.start[dy->cur ^ 1];
-  const int nd = dy->n_dirty;
-  const int w = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  for (int i = gtid() >> 5; i < nd; i += gstride() >> 5) {
-    const int32_t L = c.dirty_list[i];
-    const int32_t base = c.rng[dy->cur ^ 1][L].x;
-    const int32_t n = c.patch_count[i];
+// One dirty lane L (whole warp): its n members, sorted, to A[base, base + n).
+__device__ void patch_lane(const Ctx& c, const VRec* C, VRec* A, const int32_t* CS, int32_t L, int32_t base,
+                           int32_t n, VRec* m) {
+  const Dyn* dy = c.dyn;
+  const int lane_id = threadIdx.x & 31;
+  {
     if (n <= PD_CAP) {
       // gather: segment entries still on L, reverted into L, injected into L
-      VRec* m = sm[w];
       int k = 0;
       auto take = [&](bool mine, int32_t j) {
         const unsigned bb = __ballot_sync(0xffffffffu, mine);
@@ -2124,12 +2077,11 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_patch_dirty(Ctx c) {
   }
 }
 
-// End of regroup: C becomes the snapshot (swap the layout buffers) unless the
-// full regroup rebuilt A; the snapshot's record count and vehicle count.
-__global__ void k_patch_finish(Ctx c) {
-  PDL_WAIT();
+// Step end, once: clear the dirty marks; C becomes the snapshot (swap the
+// layout buffers) unless the full regroup rebuilt A; record and vehicle
+// counts of the new snapshot; end-of-step counters.
+__device__ void regroup_finish(const Ctx& c) {
   Dyn* dy = c.dyn;
-  // clear dirty flags and membership deltas for the next step
   for (int i = threadIdx.x; i < dy->n_dirty; i += blockDim.x) {
     c.dirty_flag[c.dirty_list[i]] = 0;
     c.cdelta[c.dirty_list[i]] = 0;
@@ -2147,13 +2099,75 @@ __global__ void k_patch_finish(Ctx c) {
       dy->n_drv = dy->n_a;
       dy->n_regroup_full++;
     }
-    // end of step counters
     dy->finished_total += dy->finished_now;
     dy->reverts_total += dy->reverts_last;
     dy->fin_log_n += dy->finished_now;
     dy->speeds_pending = 1;  // accumulated by the next step's k_speeds branch or a flush
     dy->n_own = 0;           // sharded: recounted by k_count_own
   }
+}
+
+// The next snapshot, in one launch.  Nothing changed after the sweep: C is
+// the snapshot.  Some lanes changed membership or order (dirty): C is the
+// snapshot with those lanes rebuilt into its tail, after n_c + n_inj -- every
+// block scans the dirty lanes' new member counts (C segment + the deltas the
+// revert replay and the injection recorded, cdelta) into their tail offsets,
+// block 0 publishes the lane ranges, and each warp rebuilds its lanes.  Too
+// many dirty lanes: the full regroup (COND_FULL section) instead, which also
+// ends the step.  Otherwise the last block to finish ends it.
+static constexpr int RG_BLOCKS = 296;
+__global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c) {
+  PDL_WAIT();
+  Dyn* dy = c.dyn;
+  __shared__ int32_t sd[PATCH_MAX];
+  __shared__ VRec sm[PD_WARPS][PD_CAP];
+  __shared__ int s_last;
+  const int nd = dy->n_dirty;
+  if (dy->need_regroup) {
+    if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        dy->full_regroup = 1;
+        set_cond(c, COND_FULL, true);
+      }
+      return;
+    }
+    VRec* C = c.lay[dy->cur ^ 1];  // sources [0, n_c + n_inj), destination its tail
+    const int32_t* CS = c.start[dy->cur ^ 1];
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+      const int32_t L = c.dirty_list[i];
+      sd[i] = (CS[L + 1] - CS[L]) + c.cdelta[L];
+    }
+    __syncthreads();
+    const int32_t tot = block_excl_scan<PATCH_MAX / (32 * PD_WARPS)>(sd, nd);
+    const int32_t base0 = dy->n_c + dy->n_inj;
+    if (blockIdx.x == 0) {
+      int2* R = c.rng[dy->cur ^ 1];
+      for (int i = threadIdx.x; i < nd; i += blockDim.x)
+        R[c.dirty_list[i]] = make_int2(base0 + sd[i], base0 + (i + 1 < nd ? sd[i + 1] : tot));
+      if (threadIdx.x == 0) dy->tail_n = tot;
+    }
+    const int w = threadIdx.x >> 5;
+    for (int i = blockIdx.x * PD_WARPS + w; i < nd; i += gridDim.x * PD_WARPS) {
+      const int32_t n = (i + 1 < nd ? sd[i + 1] : tot) - sd[i];
+      patch_lane(c, C, C, CS, c.dirty_list[i], base0 + sd[i], n, sm[w]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&dy->rg_done, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  regroup_finish(c);
+}
+
+// End of a step whose snapshot the full regroup rebuilt (COND_FULL section).
+__global__ void k_patch_finish(Ctx c) {
+  PDL_WAIT();
+  if (!c.dyn->full_regroup) return;  // k_regroup ended it (eager mode runs this section)
+  regroup_finish(c);
 }
 
 // ------------------------------------------------------------------ end of step
@@ -2231,6 +2245,7 @@ __global__ void k_begin_step(Ctx c) {
   dy->rf_arrive = 0;
   dy->rf_conflict = 0;
   dy->rf_done = 0;
+  dy->rg_done = 0;
 }
 
 __global__ void k_set_na(Ctx c, const int32_t* gate) {
