@@ -123,6 +123,8 @@ struct Dyn {
   int32_t rf_conflict;  // k_resolve_fast: closures overlap or exceed a budget (general path)
   int32_t rf_done;      // k_resolve_fast replayed every event
   int32_t rg_done;      // k_regroup: blocks finished (the last one ends the step)
+  int32_t rf_fin;       // k_resolve_fast: replays finished
+  int32_t pad3_;
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };

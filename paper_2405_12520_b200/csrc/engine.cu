@@ -95,6 +95,7 @@ struct tsb_engine {
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
+  cudaGraph_t else_graph = nullptr;
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
   int32_t launches_per_step = 0;
@@ -183,7 +184,7 @@ static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in
 // Conditional section (graph capture only): an IF node on handle c.cond[k]
 // whose body captures every launch until cond_end.  Outside capture both are
 // no-ops and the section's kernels gate themselves on the same flags.
-static void cond_begin(tsb_engine* e, int k) {
+static void cond_begin(tsb_engine* e, int k, bool with_else = false) {
   if (!e->capturing || !e->c.use_cond) return;
   cudaStreamCaptureStatus st;
   unsigned long long id;
@@ -195,16 +196,29 @@ static void cond_begin(tsb_engine* e, int k) {
   prm.type = cudaGraphNodeTypeConditional;
   prm.conditional.handle = e->c.cond[k];
   prm.conditional.type = cudaGraphCondTypeIf;
-  prm.conditional.size = 1;
+  prm.conditional.size = with_else ? 2 : 1;
   cudaGraphNode_t node;
   if (er == cudaSuccess) er = cudaGraphAddNode(&node, g, deps, nd, &prm);
   if (er == cudaSuccess) er = cudaStreamUpdateCaptureDependencies(e->stream, &node, 1, cudaStreamSetCaptureDependencies);
   if (er == cudaSuccess) {
     e->body_graph = prm.conditional.phGraph_out[0];
+    e->else_graph = with_else ? prm.conditional.phGraph_out[1] : nullptr;
     er = cudaStreamBeginCaptureToGraph(e->body, e->body_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   }
   if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
   e->cur = e->body;
+}
+// Switches the capture of an IF/ELSE node (cond_begin(.., true)) to its
+// else body; false outside capture (then only the IF body is issued, its
+// kernels gating themselves).
+static bool cond_else(tsb_engine* e) {
+  if (!e->capturing || !e->c.use_cond) return false;
+  cudaGraph_t done;
+  cudaError_t er = cudaStreamEndCapture(e->body, &done);
+  if (er == cudaSuccess)
+    er = cudaStreamBeginCaptureToGraph(e->body, e->else_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
+  return true;
 }
 static void cond_end(tsb_engine* e) {
   if (!e->capturing || !e->c.use_cond) return;
@@ -259,13 +273,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     cudaEventRecord(e->ev_join2, e->side2);
     e->cur = main_s;
   }
-  // exact revert resolution (only when some lane's sweep reverts)
+  // exact revert resolution: the per-event fast path; it flags the step RARE
+  // when closures meet, and when the regroup might not fit the patch
   LAUNCH(KC_RESOLVE, k_resolve_fast, RF_BLOCKS, 32 * RC_WARPS, c);
-  cond_begin(e, COND_RESOLVE);  // events whose closures meet or overflow a budget
-  LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
-  LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
-  LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
-  cond_end(e);
   if (!fork_signals) {
     if (c.p.controller == 1) {  // max-pressure reads the post-sweep lane counts
       cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->cur);
@@ -273,12 +283,19 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     }
     LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
     LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
-    LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
+    LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);  // flags the step RARE when trips are due or retrying
   } else {
     cudaStreamWaitEvent(e->cur, e->ev_join2, 0);
   }
-  // injection (only when trips are due or waiting for a retry)
-  cond_begin(e, COND_INJECT);
+  cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
+  // One IF/ELSE node (a conditional node costs ~8 us, tools/graph_overhead.cu):
+  // RARE steps run the general resolver, the injection and a regroup that may
+  // be the full one, each section's kernels gating themselves; the common
+  // step only the regroup patch.
+  cond_begin(e, COND_RARE, true);
+  LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
+  LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
+  LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
   LAUNCH(KC_INJECT, k_inject_hist, vgrid, VB, c);
   scan(e, L, KC_INJECT, SCAN_INJ_LANES, c.inj_cnt, c.inj_start, SEL_NONE, nullptr, NL, NL, &dy->n_due);
   LAUNCH(KC_INJECT, k_inject_scatter, vgrid, VB, c);
@@ -287,19 +304,17 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   scan(e, L, KC_INJECT, SCAN_INJ_RETRY, c.flag_in, c.flag_scan, SEL_NONE, &dy->n_due, 0, e->n_trips, &dy->n_due);
   LAUNCH(KC_INJECT, k_retry_compact, vgrid, VB, c);
   LAUNCH(KC_INJECT, k_inject_finish, 1, 1, c);
-  cond_end(e);
-  // next snapshot: nothing if no lane changed membership/order; else rebuild
-  // only the dirty lanes and shift the rest; full regroup if too many changed
-  cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
-  LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c);
-  cond_begin(e, COND_FULL);
-  cudaMemsetAsync(c.cnt, 0, sizeof(int32_t) * NL, e->cur);
+  // next snapshot: C as is, C with the dirty lanes rebuilt into its tail, or
+  // (too many dirty lanes) the full regroup
+  LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 1);
+  LAUNCH(KC_REGROUP, k_zero_cnt, tgrid, VB, c, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_hist, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, &dy->full_regroup);
   scan(e, L, KC_REGROUP, SCAN_REGROUP, c.cnt, nullptr, SEL_A, nullptr, NL, NL, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
+  if (cond_else(e)) LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 0);
   cond_end(e);
   if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
 }

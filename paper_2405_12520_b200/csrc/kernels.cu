@@ -71,7 +71,7 @@ __device__ __forceinline__ int2 seg(const Ctx& c, const int2* R, int32_t L) { re
 // runs only when its deciding kernel sets the handle.  The handles default to
 // 0 at every graph launch; in eager launches (profiling, host-continuation
 // mode) use_cond is 0 and the sections' kernels gate themselves instead.
-enum { COND_RESOLVE = 0, COND_INJECT = 1, COND_FULL = 2, N_COND = 3 };
+enum { COND_RARE = 0, N_COND = 1 };
 __device__ __forceinline__ void set_cond(const Ctx& c, int k, bool v) {
   if (c.use_cond && v) cudaGraphSetConditional(c.cond[k], 1u);
 }
@@ -1545,6 +1545,15 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
 // One warp per component: the replay restricted to the component's lanes.
 static constexpr int RC_WARPS = 2;
 
+// The common-step body of the step graph only patches the snapshot: when the
+// lanes changed after the sweep exceed what the patch handles, the step must
+// take the RARE body (which can run the full regroup).
+static constexpr int PATCH_MAX = 4096;  // dirty lanes (and moved vehicles) the patch handles
+__device__ void rare_if_unpatchable(const Ctx& c) {
+  const Dyn* dy = c.dyn;
+  if (dy->n_dirty > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) set_cond(c, COND_RARE, true);
+}
+
 // The common case without the closure kernel: every event's closure is
 // computed by its own warp (breadth-first over "entered member -> its
 // snapshot lane", as k_resolve_closure), lanes are claimed in rf_owner
@@ -1552,17 +1561,20 @@ static constexpr int RC_WARPS = 2;
 // component budgets, each event is a component of its own and its warp
 // replays it at once.  Otherwise nothing was modified except the claims and
 // the general path (closure, components, sequential fallback) runs in the
-// COND_RESOLVE section.  The warps of one launch wait for each other once
+// RARE body of the step graph.  The warps of one launch wait for each other once
 // (all co-resident: at most RF_BLOCKS small blocks).
 static constexpr int RF_BLOCKS = 64;
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
   const int32_t ne = dy->n_events;
-  if (ne == 0) return;
+  if (ne == 0) {
+    if (gtid() == 0) rare_if_unpatchable(c);
+    return;
+  }
   if (ne > RF_BLOCKS * RC_WARPS || (c.debug & 5)) {  // debug bit 0: sequential, bit 2: general path
     if (gtid() == 0) {
-      set_cond(c, COND_RESOLVE, true);
+      set_cond(c, COND_RARE, true);
       dy->n_resolve_general++;
     }
     return;
@@ -1656,7 +1668,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   __syncwarp();
   if (s_bad[w]) {
     if (ev == 0 && lid == 0) {
-      set_cond(c, COND_RESOLVE, true);
+      set_cond(c, COND_RARE, true);
       dy->n_resolve_general++;
     }
     return;
@@ -1690,6 +1702,12 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     const int32_t base = atomicAdd(&dy->n_moved, R.nmoved);
     for (int32_t k = 0; k < R.nmoved; k++) c.rs_moved[base + k] = R.moved[k];
     atomicAdd((unsigned long long*)&dy->reverts_last, (unsigned long long)R.reverts);
+    // the last replay to finish sees the final dirty / moved counts
+    __threadfence();
+    if (atomicAdd(&dy->rf_fin, 1) == ne - 1) {
+      __threadfence();
+      rare_if_unpatchable(c);
+    }
   }
 }
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_comp(Ctx c) {
@@ -1874,7 +1892,7 @@ __global__ void k_inject_due(Ctx c) {
     dy->n_due = nr + nn;
     dy->n_retry = 0;
     dy->injected_now = 0;
-    set_cond(c, COND_INJECT, nr + nn > 0);
+    set_cond(c, COND_RARE, nr + nn > 0);
     if (nr + nn > 0) dy->n_inject_steps++;
   }
 }
@@ -1999,7 +2017,6 @@ __global__ void k_inject_finish(Ctx c) {
 
 // ------------------------------------------------------------------ incremental regroup
 
-static constexpr int PATCH_MAX = 4096;  // dirty lanes handled by the patch path
 
 // Members of dirty lane L in the post-sweep layout C: segment entries still on
 // L, vehicles reverted into L, vehicles injected into L (C tail).
@@ -2113,10 +2130,10 @@ __device__ void regroup_finish(const Ctx& c) {
 // block scans the dirty lanes' new member counts (C segment + the deltas the
 // revert replay and the injection recorded, cdelta) into their tail offsets,
 // block 0 publishes the lane ranges, and each warp rebuilds its lanes.  Too
-// many dirty lanes: the full regroup (COND_FULL section) instead, which also
-// ends the step.  Otherwise the last block to finish ends it.
+// many dirty lanes: the full regroup (the RARE body's following kernels)
+// instead, which also ends the step.  Otherwise the last block to finish ends it.
 static constexpr int RG_BLOCKS = 296;
-__global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c) {
+__global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
   __shared__ int32_t sd[PATCH_MAX];
@@ -2126,8 +2143,10 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c) {
   if (dy->need_regroup) {
     if (nd > PATCH_MAX || dy->n_inj > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        dy->full_regroup = 1;
-        set_cond(c, COND_FULL, true);
+        if (may_full)
+          dy->full_regroup = 1;  // the full regroup kernels follow in this body
+        else
+          dy->overflow |= 32;  // common body without the full regroup: rare_if_unpatchable missed it
       }
       return;
     }
@@ -2163,7 +2182,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c) {
   regroup_finish(c);
 }
 
-// End of a step whose snapshot the full regroup rebuilt (COND_FULL section).
+// End of a step whose snapshot the full regroup rebuilt.
 __global__ void k_patch_finish(Ctx c) {
   PDL_WAIT();
   if (!c.dyn->full_regroup) return;  // k_regroup ended it (eager mode runs this section)
@@ -2246,6 +2265,13 @@ __global__ void k_begin_step(Ctx c) {
   dy->rf_conflict = 0;
   dy->rf_done = 0;
   dy->rg_done = 0;
+  dy->rf_fin = 0;
+}
+
+__global__ void k_zero_cnt(Ctx c, const int32_t* gate) {
+  PDL_WAIT();
+  if (gated_off(gate)) return;
+  for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) c.cnt[L] = 0;
 }
 
 __global__ void k_set_na(Ctx c, const int32_t* gate) {
