@@ -1554,6 +1554,185 @@ __device__ void rare_if_unpatchable(const Ctx& c) {
   if (dy->n_dirty > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) set_cond(c, COND_RARE, true);
 }
 
+// Fast-path replay on chip.  Every vehicle that can be on a closure lane
+// during the replay is a member of some closure lane's C segment (a revert
+// only moves a vehicle back to its snapshot lane, which is in the closure),
+// so the warp stages all of them once, during the closure search, and the
+// replay reads and updates the staged copy, writing every change through to
+// C (the lanes are this warp's alone: claimed).  Same algorithm, same
+// arithmetic as replay() / resolve_lane().
+static constexpr int RF_CACHE = 192;
+struct RfE {
+  double s, v, snap_s;
+  int32_t j, vix, lane, snap_lane, snap_rptr, src;
+  int32_t reverted, pad;
+};
+struct RfSmem {
+  union {
+    struct {
+      RsM m[RS_CAP];
+      RsM t[RS_CAP];
+    } g;  // global-gather replay (closure larger than the cache)
+    struct {
+      RfE e[RF_CACHE];
+      int16_t i1[RF_CACHE], i2[RF_CACHE];
+    } k;
+  };
+};
+
+// resolve_lane() on the staged members; returns the cache index of the
+// vehicle to revert, or -1 (same value in every thread).
+__device__ int32_t resolve_lane_cached(const Ctx& c, VRec* C, int32_t L, RfE* E, int32_t ncache, int16_t* i1,
+                                       int16_t* i2) {
+  const int lid = threadIdx.x & 31;
+  const Params& p = c.p;
+  int n = 0;
+  for (int32_t base = 0; base < ncache; base += 32) {
+    const int32_t k = base + lid;
+    const bool mine = k < ncache && E[k].lane == L;
+    const unsigned b = __ballot_sync(0xffffffffu, mine);
+    if (mine) i1[n + __popc(b & ((1u << lid) - 1))] = (int16_t)k;
+    n += __popc(b);
+  }
+  __syncwarp();
+  for (int a = lid; a < n; a += 32) {
+    const RfE& x = E[i1[a]];
+    int rank = 0;
+    for (int b2 = 0; b2 < n; b2++) rank += ahead_of(E[i1[b2]].s, E[i1[b2]].vix, x.s, x.vix) ? 1 : 0;
+    i2[rank] = i1[a];
+  }
+  __syncwarp();
+  int32_t rev = -1;
+  if (lid == 0) {
+    int prev = -1;
+    double prev_rear = CUDART_INF;
+    for (int a = 0; a < n; a++) {
+      RfE& x = E[i2[a]];
+      const double limit = prev_rear - p.s0_floor;
+      const bool entered = x.snap_lane != L;
+      if (x.s > limit + 1e-12) {
+        const double floor_s = entered ? 0.0 : x.snap_s;
+        if (limit >= floor_s) {
+          x.v = py_max(0.0, py_min(x.v, x.v - (x.s - limit) / p.dt));
+          x.s = limit;
+        } else if (entered && !x.reverted) {
+          rev = i2[a];
+          break;
+        } else if (prev >= 0 && E[i2[prev]].snap_lane != L && !E[i2[prev]].reverted) {
+          rev = i2[prev];
+          break;
+        } else {
+          x.v = 0.0;
+          x.s = floor_s;
+        }
+      }
+      prev = a;
+      prev_rear = x.s - p.L;
+    }
+  }
+  __syncwarp();
+  for (int a = lid; a < n; a += 32) {
+    const RfE& x = E[i2[a]];
+    C[x.j].s = x.s;
+    C[x.j].v = x.v;
+  }
+  rev = __shfl_sync(0xffffffffu, rev, 0);
+  __syncwarp();
+  return rev;
+}
+
+// replay() on the staged members, with the per-lane replay flags on chip
+// too (closure lanes q[0, qn), flags fl[]; E = the one event lane).
+enum : uint8_t { RF_INWORK = 1, RF_TOUCHED = 2 };
+__device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& R, RfE* E, int32_t ncache,
+                              int16_t* i1, int16_t* i2, const int32_t* q, uint8_t* fl, int32_t ev_lane,
+                              int64_t max_reverts) {
+  const int lid = threadIdx.x & 31;
+  auto qi = [&](int32_t x) {
+    int k = 0;
+    while (q[k] != x) k++;
+    return k;
+  };
+  for (;;) {
+    int32_t L = -1;
+    if (lid == 0) {
+      while (R.hn > 0) {
+        const int32_t x = heap_pop(R.heap, R.hn);
+        uint8_t& f = fl[qi(x)];
+        if (!(f & RF_INWORK)) continue;
+        f &= ~RF_INWORK;
+        if (!(f & RF_TOUCHED)) {
+          f |= RF_TOUCHED;
+          R.touched[R.nt++] = x;
+        }
+        if (c.sharded) R.zf |= ((c.zone[x] & ZF_OWN) ? 1 : 0) | ((c.zone[x] & ZF_EXACT) ? 0 : 2);
+        if (x > R.reach) R.reach = x;
+        L = x;
+        break;
+      }
+    }
+    L = __shfl_sync(0xffffffffu, L, 0);
+    if (L < 0) break;
+    const int32_t rk = resolve_lane_cached(c, C, L, E, ncache, i1, i2);
+    if (rk < 0) continue;
+    // _revert (world.py:501-507) and rescheduling
+    const int32_t Lb = E[rk].snap_lane;
+    int restore = 0, stop = 0;
+    if (lid == 0) {
+      R.reverts++;
+      RfE& x = E[rk];
+      x.lane = Lb;
+      x.s = x.snap_s;
+      x.v = 0.0;
+      x.reverted = 1;
+      VRec& r = C[x.j];
+      r.lane = Lb;
+      r.s = x.snap_s;
+      r.v = 0.0;
+      r.rptr = x.snap_rptr;
+      R.moved[R.nmoved++] = x.j;
+      atomicAdd(&c.cdelta[L], -1);  // membership change for the regroup
+      atomicAdd(&c.cdelta[Lb], 1);
+      uint8_t& fb = fl[qi(Lb)];
+      if (!(fb & RF_TOUCHED)) {
+        fb |= RF_TOUCHED;
+        R.touched[R.nt++] = Lb;
+        // the reference sweeps Lb for the first time only now, with the
+        // reverted vehicle present: undo k_lanesort's tentative sweep
+        restore = (Lb > R.reach && Lb != ev_lane) ? 1 : 0;
+      }
+      uint8_t& fa = fl[qi(L)];
+      if (!(fa & RF_INWORK)) {
+        fa |= RF_INWORK;
+        heap_push(R.heap, R.hn, L);
+      }
+      if (!(fb & RF_INWORK)) {
+        fb |= RF_INWORK;
+        heap_push(R.heap, R.hn, Lb);
+      }
+      stop = R.reverts >= max_reverts;  // the reference's pass bound (world.py:518)
+    }
+    restore = __shfl_sync(0xffffffffu, restore, 0);
+    __syncwarp();
+    if (restore) {
+      // Lb's C segment members: the staged entries whose C index lies in it
+      const int32_t lo = CS[Lb], hi = CS[Lb + 1];
+      for (int32_t k = lid; k < ncache; k += 32) {
+        RfE& x = E[k];
+        if (x.j >= lo && x.j < hi) {
+          const VRec o = c.B[x.src];
+          x.s = o.s;
+          x.v = o.v;
+          C[x.j].s = o.s;
+          C[x.j].v = o.v;
+        }
+      }
+    }
+    __syncwarp();
+    if (__shfl_sync(0xffffffffu, stop, 0)) break;
+  }
+}
+
 // The common case without the closure kernel: every event's closure is
 // computed by its own warp (breadth-first over "entered member -> its
 // snapshot lane", as k_resolve_closure), lanes are claimed in rf_owner
@@ -1582,16 +1761,16 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int32_t ev = blockIdx.x * RC_WARPS + w;
   if (ev >= ne) return;
-  __shared__ RsM sm[RC_WARPS][RS_CAP];
-  __shared__ RsM st[RC_WARPS][RS_CAP];
-  __shared__ int32_t sh[RC_WARPS][HCAP], smv[RC_WARPS][2 * HCAP], stl[RC_WARPS][HCAP];
+  __shared__ RfSmem U[RC_WARPS];
+  __shared__ int32_t sh[RC_WARPS][HCAP], smv[RC_WARPS][2 * HCAP], stl[RC_WARPS][HCAP], sq[RC_WARPS][HCAP];
+  __shared__ uint8_t sfl[RC_WARPS][HCAP];
   __shared__ int32_t s_bad[RC_WARPS];
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
   const VRec* A = c.lay[dy->cur];
   const unsigned long long mine = ((unsigned long long)(uint32_t)(dy->step_no + 1) << 32) | (uint32_t)(ev + 1);
   const unsigned long long epoch = mine >> 32;
-  int32_t* q = stl[w];  // closure lanes (the touched list is filled only later, by the replay)
+  int32_t* q = sq[w];  // closure lanes
   // claim lane T for this closure: 1 new, 0 already ours, -1 another closure's
   auto claim = [&](int32_t T) -> int {
     unsigned long long old = c.rf_owner[T];
@@ -1607,7 +1786,8 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
 #endif
   const int32_t E = c.events[ev];
-  int32_t qn = 1, nedge = 0;
+  int32_t qn = 1, nedge = 0, ncache = 0;  // ncache > RF_CACHE: not staged (global replay)
+  RfE* cache = U[w].k.e;
   bool bad = false;
   if (lid == 0) {
     q[0] = E;
@@ -1620,29 +1800,33 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     for (int32_t b0 = j0; b0 < j1; b0 += 32) {
       const int32_t j = b0 + lid;
       int32_t T = L;
-      if (j < j1) T = A[C[j].src].lane;
+      VRec r, sn;
+      if (j < j1) {
+        r = C[j];
+        sn = A[r.src];
+        T = sn.lane;
+      }
+      // stage the member for the replay
+      const unsigned vm = __ballot_sync(0xffffffffu, j < j1);
+      const int slot = ncache + __popc(vm & ((1u << lid) - 1));
+      if (j < j1 && slot < RF_CACHE)
+        cache[slot] = RfE{r.s, r.v, sn.s, j, r.vix, L, sn.lane, sn.rptr, r.src, 0, 0};
+      ncache += __popc(vm);
       const bool entered = T != L;
       const unsigned em = __ballot_sync(0xffffffffu, entered);
       nedge += __popc(em);
-      // append newly claimed origin lanes, one lane at a time (few per lane)
-      unsigned pend = em;
-      while (pend) {
-        const int src_l = __ffs(pend) - 1;
-        pend &= pend - 1;
-        const int32_t Tk = __shfl_sync(0xffffffffu, T, src_l);
-        int r = 0;
-        if (lid == 0) r = claim(Tk);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        if (r < 0) bad = true;
-        if (r == 1) {
-          if (qn >= HCAP) {
-            bad = true;
-          } else {
-            if (lid == 0) q[qn] = Tk;
-            qn++;
-          }
-        }
+      // claim the origin lanes of the entered members, all at once (two
+      // members from one lane: one claims it, the other finds it ours)
+      const int cr = entered ? claim(T) : 0;
+      if (__any_sync(0xffffffffu, cr < 0)) bad = true;
+      const unsigned nm = __ballot_sync(0xffffffffu, cr == 1);
+      if (qn + __popc(nm) > HCAP) {
+        bad = true;
+      } else if (cr == 1) {
+        q[qn + __popc(nm & ((1u << lid) - 1))] = T;
       }
+      qn += __popc(nm);
+      if (qn > HCAP) qn = HCAP;
     }
     // on-chip budget: a lane's members plus every edge of the closure (a
     // bound on the vehicles that can be reverted into it)
@@ -1678,9 +1862,15 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     dy->n_resolve_fast++;
   }
   Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
+  const bool staged = ncache <= RF_CACHE;
   if (lid == 0) {
-    c.rs_event[E] = 1;
-    c.rs_inwork[E] = 1;
+    if (staged) {
+      for (int k = 0; k < qn; k++) sfl[w][k] = 0;
+      sfl[w][0] = RF_INWORK;  // q[0] == E
+    } else {
+      c.rs_event[E] = 1;
+      c.rs_inwork[E] = 1;
+    }
     heap_push(R.heap, R.hn, E);
   }
   __syncwarp();
@@ -1688,7 +1878,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   unsigned long long t2;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
 #endif
-  replay(c, C, CS, A, R, sm[w], st[w], (int64_t)dy->n_c + 2);
+  if (staged)
+    replay_cached(c, C, CS, R, cache, ncache, U[w].k.i1, U[w].k.i2, q, sfl[w], E, (int64_t)dy->n_c + 2);
+  else
+    replay(c, C, CS, A, R, U[w].g.m, U[w].g.t, (int64_t)dy->n_c + 2);
 #ifdef TSB_RF_TRACE
   unsigned long long t3;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
@@ -1697,7 +1890,11 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
            (long long)dy->step_no, ev, ne, E, qn, nedge, R.nt, (long long)R.reverts, t1 - t0, t2 - t1, t3 - t2);
 #endif
   if (lid == 0) {
-    replay_finish(c, R);
+    if (staged) {
+      for (int32_t k = 0; k < R.nt; k++) mark_dirty(c, R.touched[k]);  // no global flags to clear
+    } else {
+      replay_finish(c, R);
+    }
     if (c.sharded && R.zf == 3) dy->overflow |= 16;
     const int32_t base = atomicAdd(&dy->n_moved, R.nmoved);
     for (int32_t k = 0; k < R.nmoved; k++) c.rs_moved[base + k] = R.moved[k];

@@ -1,4 +1,3 @@
-# resolve fast-path phase timing (globaltimer printf variant) + bench with path counters
+# resolve fast-path phase timing (globaltimer printf variant)
 mkdir -p gpurun_out
 TSB200_LIB=$PWD/build_variants/lib_rftrace.so timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/rf_trace.log 2>&1; echo trace rc $?
-TSB200_LIB=$PWD/build_variants/lib_cnt.so timeout 600 python bench.py --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/rf_cnt.log 2>&1; echo cnt rc $?
