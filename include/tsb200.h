@@ -200,7 +200,8 @@ int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
 /* Test knobs: bit 0 forces the sequential revert-chain resolver, bit 1 the
  * full (non-incremental) regroup, bit 2 the general (closure + components)
  * resolver instead of the per-event fast path, bit 3 a step graph without
- * conditional nodes (every section's kernels launched, gating themselves).
+ * conditional nodes (every section's kernels launched, gating themselves),
+ * bit 4 the parallel branches at default (not highest) priority.
  * Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);
 /* Which step paths ran so far (measurement hook): out[0] steps whose revert
@@ -209,6 +210,11 @@ int tsb_set_debug(tsb_engine* e, int32_t flags);
  * full regroups, out[4] steps that ran the injection section. */
 #define TSB_PATH_COUNTERS 5
 int tsb_path_counters(tsb_engine* e, int64_t* out);
+/* Step timeline (libraries built with -DTSB_TIMELINE, else TSB_EINVAL):
+ * out[64 * 16] = %globaltimer stamps (ns) of the last 64 steps, a ring of
+ * rows, slot = phase (kernels.cu TL_*), taken when the phase's kernel
+ * passed its dependency wait. */
+int tsb_timeline(tsb_engine* e, uint64_t* out);
 /* Kernel launches issued per step (for the bench's gpu_launches claim). */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);
 

@@ -47,6 +47,7 @@ SIGNATURES = {
     "tsb_launches_per_step": (_i32, [_vp, C.POINTER(_i32)]),
     "tsb_set_debug": (_i32, [_vp, _i32]),
     "tsb_path_counters": (_i32, [_vp, _vp]),
+    "tsb_timeline": (_i32, [_vp, _vp]),
     "tsb_create_sharded": (_i32, [_vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
     "tsb_mark": (_i32, [_vp, _i32]),
     "tsb_set_pow_mode": (_i32, [_vp, _i32]),

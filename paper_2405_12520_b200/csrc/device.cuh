@@ -124,7 +124,7 @@ struct Dyn {
   int32_t rf_done;      // k_resolve_fast replayed every event
   int32_t rg_done;      // k_regroup: blocks finished (the last one ends the step)
   int32_t rf_fin;       // k_resolve_fast: replays finished
-  int32_t pad3_;
+  int32_t tl_row;       // TSB_TIMELINE builds: the step's row in the timeline ring
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };
@@ -262,6 +262,7 @@ struct Ctx {
   int32_t n_win;
   int32_t* hostq;
   Dyn* dyn;
+  unsigned long long* tl;  // TSB_TIMELINE builds: 64 x 16 step timestamps
   double* scratch_d;
 };
 

@@ -92,6 +92,7 @@ struct tsb_engine {
   cudaStream_t side = nullptr;  // parallel branch (road aggregate)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side2 = nullptr;  // parallel branch (signals, clock, due list)
+  int prio_hi = 0;               // greatest stream priority of the device
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
@@ -153,24 +154,34 @@ struct Launcher {
 // Launched with programmatic stream serialization (PDL, see kernels.cu
 // PDL_WAIT): the next kernel's launch overlaps the previous kernel's tail.
 template <class... KArgs, class... Args>
-static void launch_pdl(cudaStream_t st, dim3 grid, dim3 block, void (*kern)(KArgs...), Args&&... args) {
-  cudaLaunchAttribute attr[1];
+static void launch_pdl(cudaStream_t st, int prio, dim3 grid, dim3 block, void (*kern)(KArgs...), Args&&... args) {
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = prio;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = prio ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Kernels of the parallel branches run at the device's highest priority: they
+// then take SM slots as the update's blocks retire instead of stretching the
+// latency-bound scan / placement that follow it (debug bit 4 turns this off).
+static int side_prio(const tsb_engine* e) {
+  if (e->c.debug & 16) return 0;
+  return (e->cur == e->side || e->cur == e->side2) ? e->prio_hi : 0;
 }
 
 #define LAUNCH(kc, kern, grid, block, ...)                          \
   do {                                                              \
     L.pre(kc);                                                      \
-    launch_pdl(e->cur, dim3(grid), dim3(block), kern, __VA_ARGS__); \
+    launch_pdl(e->cur, side_prio(e), dim3(grid), dim3(block), kern, __VA_ARGS__); \
     L.post();                                                       \
   } while (0)
 
@@ -243,9 +254,12 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     // previous step's road aggregate on a parallel branch (joined before the regroup)
     cudaEventRecord(e->ev_fork, e->cur);
     cudaStreamWaitEvent(e->side, e->ev_fork, 0);
-    L.pre(KC_SPEEDS);
-    k_speeds<<<grid_for((int64_t)std::max(e->n_roads, 1) * 32, VB, 1 << 30), VB, 0, e->side>>>(c, 0);
-    L.post();
+    {
+      cudaStream_t main_s = e->cur;
+      e->cur = e->side;
+      LAUNCH(KC_SPEEDS, k_speeds, grid_for(std::max(e->n_roads, 1), 128, 1 << 30), 128, c, 0);
+      e->cur = main_s;
+    }
     cudaEventRecord(e->ev_join, e->side);
     if (c.p.pow_glibc)
       LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
@@ -322,7 +336,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
 // Accumulates the current snapshot's road aggregate if the next step has not
 // done it yet (k_speeds); called before the aggregate is read.
 static int flush_speeds(tsb_engine* e) {
-  k_speeds<<<grid_for((int64_t)std::max(e->n_roads, 1) * 32, 256, 1 << 30), 256, 0, e->stream>>>(e->c, 1);
+  k_speeds<<<grid_for(std::max(e->n_roads, 1), 128, 1 << 30), 128, 0, e->stream>>>(e->c, 1);
   k_speeds_done<<<1, 1, 0, e->stream>>>(e->c);
   CK(cudaGetLastError());
   return TSB_OK;
@@ -696,6 +710,11 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   CK(cudaStreamCreateWithFlags(&e->body, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    e->prio_hi = hi;
+  }
   CK(cudaEventCreateWithFlags(&e->ev_fork2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_join2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
@@ -945,6 +964,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.rs_touched, NL));
   RC(dalloc(E, &c.rs_event, NL));
   RC(dalloc(E, &c.rf_owner, NL));
+  RC(dalloc(E, &c.tl, 64 * 16));
   RC(dalloc(E, &c.rs_movedin, NL));
   RC(dalloc(E, &c.rs_moved, CAP));
   RC(dalloc(E, &c.rs_reverted, CAP));
@@ -1351,6 +1371,18 @@ int tsb_set_debug(tsb_engine* e, int32_t flags) {
   e->c.debug = flags;
   e->graph_dirty = true;
   return TSB_OK;
+}
+
+int tsb_timeline(tsb_engine* e, uint64_t* out) {
+#ifdef TSB_TIMELINE
+  RC(sync_dyn(e));
+  CK(cudaMemcpy(out, e->c.tl, sizeof(uint64_t) * 64 * 16, cudaMemcpyDeviceToHost));
+  return TSB_OK;
+#else
+  (void)e;
+  (void)out;
+  return fail(TSB_EINVAL, "library built without -DTSB_TIMELINE");
+#endif
 }
 
 int tsb_path_counters(tsb_engine* e, int64_t* out) {

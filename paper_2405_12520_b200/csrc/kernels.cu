@@ -36,6 +36,27 @@ static constexpr double EPS_GAP = 1e-6;  // world.py:43
 // grid (and its memory) before anything is read.  No-op without the attribute.
 #define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 
+// Step timeline (measurement builds, -DTSB_TIMELINE): block 0 of a kernel
+// stamps %globaltimer once its predecessors completed (after PDL_WAIT), into
+// slot k of the current step's row of c.tl (64 steps x TL_SLOTS, a ring).
+static constexpr int TL_SLOTS = 16;
+enum { TL_BEGIN, TL_UPDATE, TL_SCAN, TL_PLACE, TL_LANEFIX, TL_RESOLVE, TL_REGROUP, TL_END, TL_SPEEDS, TL_SIGNALS,
+       TL_INJECT_DUE, TL_SPEEDS_END };
+#ifdef TSB_TIMELINE
+#define TL_MARK(k)                                                                        \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                            \
+      unsigned long long t_;                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+      c.tl[(size_t)(c.dyn->tl_row & 63) * TL_SLOTS + (k)] = t_;                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define TL_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
 
@@ -229,6 +250,7 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 template <bool G>
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_UPDATE);
   Dyn* dy = c.dyn;
   const int32_t n_a = dy->n_a;
   const int32_t n = n_a + (c.sharded ? dy->n_g : 0);
@@ -603,6 +625,7 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
                                              const int32_t* n_dev, int32_t n_static, int32_t ntiles,
                                              const int32_t* gate) {
   PDL_WAIT();
+  if (site == SCAN_LANES) TL_MARK(TL_SCAN);
   if (gated_off(gate)) return;
   int2* rng = nullptr;
   if (out_sel != SEL_NONE) {
@@ -655,27 +678,37 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
   const int32_t warp_excl = warp ? s_warp[warp - 1] : 0;
   const int32_t total = s_warp[BT / 32 - 1];
   int32_t excl = warp_excl + x - local;
-  if (threadIdx.x == 0) {
-    // status word: epoch (30 bits) | flag (2 bits) | value (32 bits);
-    // flag 1 = tile aggregate, 2 = inclusive prefix
-    volatile unsigned long long* st = status;
-    if (tile == 0) {
+  // status word: epoch (30 bits) | flag (2 bits) | value (32 bits);
+  // flag 1 = tile aggregate, 2 = inclusive prefix
+  volatile unsigned long long* st = status;
+  if (tile == 0) {
+    if (threadIdx.x == 0) {
       __threadfence();
       st[0] = ep | (2ULL << 32) | (unsigned)total;
       s_prefix = 0;
-    } else {
-      st[tile] = ep | (1ULL << 32) | (unsigned)total;
-      __threadfence();
-      int32_t acc = 0;
-      int32_t t = tile - 1;
-      for (;;) {
-        const unsigned long long w = st[t];
-        if ((w >> 34) != (ep >> 34)) continue;  // not yet published in this invocation
-        const unsigned flag = (unsigned)(w >> 32) & 3u;
-        acc += (int32_t)(unsigned)(w & 0xffffffffULL);
-        if (flag == 2) break;
-        t--;
+    }
+  } else if (warp == 0) {
+    if (lane == 0) st[tile] = ep | (1ULL << 32) | (unsigned)total;
+    __threadfence();
+    // warp-wide look-back: 32 predecessors per round, nearest first
+    int32_t acc = 0;
+    int32_t t = tile - 1;
+    for (;;) {
+      const int32_t idx = t - lane;
+      unsigned long long w = idx >= 0 ? st[idx] : (ep | (2ULL << 32));
+      while (!__all_sync(0xffffffffu, (w >> 34) == (ep >> 34))) {  // wait for the window to publish
+        if ((w >> 34) != (ep >> 34)) w = st[idx];
       }
+      const unsigned incl = __ballot_sync(0xffffffffu, ((unsigned)(w >> 32) & 3u) == 2u);
+      const int last = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive prefix ends the walk
+      int32_t pv = lane <= last ? (int32_t)(unsigned)(w & 0xffffffffULL) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+      acc += pv;
+      if (incl) break;
+      t -= 32;
+    }
+    if (lane == 0) {
       __threadfence();
       st[tile] = ep | (2ULL << 32) | (unsigned)(acc + total);
       s_prefix = acc;
@@ -848,6 +881,7 @@ __device__ __forceinline__ void flag_lane(const Ctx& c, int32_t L) {
 
 __global__ void k_place(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_PLACE);
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
@@ -921,6 +955,7 @@ static constexpr int LX_CAP = 64;   // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_LANEFIX);
   __shared__ VRec s_in[LX_WARPS][LX_CAP];
   __shared__ VRec s_out[LX_WARPS][LX_CAP];
   Dyn* dy = c.dyn;
@@ -1745,6 +1780,7 @@ __device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& 
 static constexpr int RF_BLOCKS = 64;
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_RESOLVE);
   Dyn* dy = c.dyn;
   const int32_t ne = dy->n_events;
   if (ne == 0) {
@@ -1997,6 +2033,7 @@ __global__ void k_lane_counts(Ctx c) {
 // world.py:619-647 (+ time/step increment, world.py:677-678).
 __global__ void k_signals(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_SIGNALS);
   const Params& p = c.p;
   for (int32_t j = gtid(); j < c.n_junc; j += gstride()) {
     if (!c.junc_signal[j]) continue;
@@ -2063,6 +2100,7 @@ __global__ void k_conn_flags(Ctx c) {
 // Build the due list: retry (in due order) ++ pending with departure <= time.
 __global__ void k_inject_due(Ctx c) {
   PDL_WAIT();
+  TL_MARK(TL_INJECT_DUE);
   Dyn* dy = c.dyn;
   __shared__ int32_t s_new;
   const int32_t nr = dy->n_retry;
@@ -2332,6 +2370,7 @@ __device__ void regroup_finish(const Ctx& c) {
 static constexpr int RG_BLOCKS = 296;
 __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) {
   PDL_WAIT();
+  TL_MARK(TL_REGROUP);
   Dyn* dy = c.dyn;
   __shared__ int32_t sd[PATCH_MAX];
   __shared__ VRec sm[PD_WARPS][PD_CAP];
@@ -2377,6 +2416,13 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) 
   if (!s_last) return;
   __threadfence();
   regroup_finish(c);
+#ifdef TSB_TIMELINE
+  if (threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    c.tl[(size_t)(c.dyn->tl_row & 63) * TL_SLOTS + TL_END] = t_;
+  }
+#endif
 }
 
 // End of a step whose snapshot the full regroup rebuilt.
@@ -2389,18 +2435,16 @@ __global__ void k_patch_finish(Ctx c) {
 // ------------------------------------------------------------------ end of step
 
 
-// Per road, over the new snapshot: sum v and count (world.py:649-657).
-// Warp per road, fixed-order tree reduction (deterministic).
 // Road aggregate (world.py:649-657) of a step's final snapshot A: per road,
-// sum of v and count over its lanes.  Road lanes are consecutive ids
-// (network.py:422-442), so a road's vehicles are the contiguous range
-// [S[first lane], S[last lane + 1]) of A: warp per road, fixed-order tree
-// reduction (deterministic).  In the step graph this runs at the start of the
-// NEXT step on a parallel branch (A is only read until that step's regroup,
-// which joins it), hiding it behind the update; mode 1 is the flush a query
-// issues between steps.  Both use the same order.
+// sum of v and count over its lanes (road lanes are consecutive ids,
+// network.py:422-442; each lane's records are the range seg() gives), in a
+// fixed order (deterministic).  In the step graph this runs at the start of
+// the NEXT step on a parallel branch (A is only read until that step's
+// regroup, which joins it); mode 1 is the flush a query issues between
+// steps.  Both use the same order.
 __global__ void k_speeds(Ctx c, int flush) {
   PDL_WAIT();
+  if (!flush) TL_MARK(TL_SPEEDS);
   Dyn* dy = c.dyn;
   if (!(flush ? dy->speeds_pending : dy->acc_now)) return;
   const VRec* A = c.lay[dy->cur];
@@ -2410,26 +2454,23 @@ __global__ void k_speeds(Ctx c, int flush) {
     if (gtid() == 0) dy->overflow |= 2;
     return;
   }
-  const int lane_id = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int32_t r = gtid() >> 5; r < c.n_roads; r += warps) {
+  // thread per road: a handful of lanes with a few dozen vehicles; every
+  // load of the road is independent of the others (two dependent levels:
+  // lane ranges, then speeds), summed in lane and snapshot order
+  for (int32_t r = gtid(); r < c.n_roads; r += gstride()) {
     const int2 span = c.road_span[r];
     if (c.sharded && !(c.zone[span.x] & ZF_OWN)) continue;  // the owner accumulates it
     double sum = 0.0;
     int32_t cnt = 0;
     for (int32_t L = span.x; L <= span.y; L++) {
       const int2 sg = seg(c, S, L);
-      for (int32_t j = sg.x + lane_id; j < sg.y; j += 32) sum += A[j].v;
+      for (int32_t j = sg.x; j < sg.y; j++) sum += __ldg(&A[j].v);
       cnt += sg.y - sg.x;
     }
     if (cnt == 0) continue;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane_id == 0) {
-      const size_t cell = (size_t)r * c.n_win + wi;
-      c.acc_sum[cell] += sum;
-      c.acc_cnt[cell] += cnt;
-    }
+    const size_t cell = (size_t)r * c.n_win + wi;
+    c.acc_sum[cell] += sum;
+    c.acc_cnt[cell] += cnt;
   }
 }
 
@@ -2441,6 +2482,10 @@ __global__ void k_begin_step(Ctx c) {
   PDL_WAIT();
   for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) c.cnt[L] = 0;
   if (gtid() != 0) return;
+#ifdef TSB_TIMELINE
+  c.dyn->tl_row += 1;
+  TL_MARK(TL_BEGIN);
+#endif
   Dyn* dy = c.dyn;
   dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_drv;
   dy->finished_now = 0;
