@@ -201,7 +201,8 @@ int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
  * full (non-incremental) regroup, bit 2 the general (closure + components)
  * resolver instead of the per-event fast path, bit 3 a step graph without
  * conditional nodes (every section's kernels launched, gating themselves),
- * bit 4 the parallel branches at default (not highest) priority.
+ * bit 4 the parallel branches at default (not highest) priority, bit 5
+ * one graph replay per step (no multi-step batch graph).
  * Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);
 /* Which step paths ran so far (measurement hook): out[0] steps whose revert

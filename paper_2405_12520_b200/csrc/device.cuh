@@ -125,6 +125,8 @@ struct Dyn {
   int32_t rg_done;      // k_regroup: blocks finished (the last one ends the step)
   int32_t rf_fin;       // k_resolve_fast: replays finished
   int32_t tl_row;       // TSB_TIMELINE builds: the step's row in the timeline ring
+  int32_t rare;         // the step takes the RARE body (set_rare)
+  int32_t pad4_;
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };

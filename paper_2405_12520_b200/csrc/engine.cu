@@ -87,16 +87,20 @@ struct tsb_engine {
   bool graph_dirty = true;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph4 = nullptr;       // STEPS_PER_BATCH steps
+  cudaGraphExec_t gexec4 = nullptr;
   cudaStream_t cur = nullptr;   // launch stream (see LAUNCH)
   cudaStream_t body = nullptr;  // captures conditional-section bodies
   cudaStream_t side = nullptr;  // parallel branch (road aggregate)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side2 = nullptr;  // parallel branch (signals, clock, due list)
   int prio_hi = 0;               // greatest stream priority of the device
+  cudaStream_t side3 = nullptr;  // parallel branch (the RARE body's IF node)
+  cudaStream_t cond_on = nullptr;  // stream a conditional node is being captured on
+  cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
-  cudaGraph_t else_graph = nullptr;
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
   int32_t launches_per_step = 0;
@@ -195,47 +199,35 @@ static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in
 // Conditional section (graph capture only): an IF node on handle c.cond[k]
 // whose body captures every launch until cond_end.  Outside capture both are
 // no-ops and the section's kernels gate themselves on the same flags.
-static void cond_begin(tsb_engine* e, int k, bool with_else = false) {
+static void cond_begin(tsb_engine* e, int k) {
   if (!e->capturing || !e->c.use_cond) return;
   cudaStreamCaptureStatus st;
   unsigned long long id;
   cudaGraph_t g;
   const cudaGraphNode_t* deps;
   size_t nd;
-  cudaError_t er = cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd);
+  e->cond_on = e->cur;  // the stream the node is captured on
+  cudaError_t er = cudaStreamGetCaptureInfo(e->cond_on, &st, &id, &g, &deps, &nd);
   cudaGraphNodeParams prm = {};
   prm.type = cudaGraphNodeTypeConditional;
   prm.conditional.handle = e->c.cond[k];
   prm.conditional.type = cudaGraphCondTypeIf;
-  prm.conditional.size = with_else ? 2 : 1;
+  prm.conditional.size = 1;
   cudaGraphNode_t node;
   if (er == cudaSuccess) er = cudaGraphAddNode(&node, g, deps, nd, &prm);
-  if (er == cudaSuccess) er = cudaStreamUpdateCaptureDependencies(e->stream, &node, 1, cudaStreamSetCaptureDependencies);
+  if (er == cudaSuccess) er = cudaStreamUpdateCaptureDependencies(e->cond_on, &node, 1, cudaStreamSetCaptureDependencies);
   if (er == cudaSuccess) {
     e->body_graph = prm.conditional.phGraph_out[0];
-    e->else_graph = with_else ? prm.conditional.phGraph_out[1] : nullptr;
     er = cudaStreamBeginCaptureToGraph(e->body, e->body_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   }
   if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
   e->cur = e->body;
 }
-// Switches the capture of an IF/ELSE node (cond_begin(.., true)) to its
-// else body; false outside capture (then only the IF body is issued, its
-// kernels gating themselves).
-static bool cond_else(tsb_engine* e) {
-  if (!e->capturing || !e->c.use_cond) return false;
-  cudaGraph_t done;
-  cudaError_t er = cudaStreamEndCapture(e->body, &done);
-  if (er == cudaSuccess)
-    er = cudaStreamBeginCaptureToGraph(e->body, e->else_graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
-  if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
-  return true;
-}
 static void cond_end(tsb_engine* e) {
   if (!e->capturing || !e->c.use_cond) return;
   cudaError_t er = cudaStreamEndCapture(e->body, &e->body_graph);
   if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
-  e->cur = e->stream;
+  e->cur = e->cond_on;
 }
 
 // phase 0 = whole step; 1 = through k_update; 2 = the rest (split mode).
@@ -302,11 +294,20 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     cudaStreamWaitEvent(e->cur, e->ev_join2, 0);
   }
   cudaStreamWaitEvent(e->cur, e->ev_join, 0);  // k_speeds read the old snapshot A
-  // One IF/ELSE node (a conditional node costs ~8 us, tools/graph_overhead.cu):
-  // RARE steps run the general resolver, the injection and a regroup that may
-  // be the full one, each section's kernels gating themselves; the common
-  // step only the regroup patch.
-  cond_begin(e, COND_RARE, true);
+  // The RARE body (general resolver, injection, a regroup that may be the
+  // full one; its kernels gate themselves) sits in an IF node on a parallel
+  // branch, and the common step's regroup patch on the main one: a
+  // conditional node costs ~8 us even when false (tools/graph_overhead.cu),
+  // hidden there behind the patch.  Exactly one of the two k_regroup
+  // launches works (dy->rare).
+  const bool fork_rare = e->capturing && c.use_cond;
+  cudaStream_t main_s = e->cur;
+  if (fork_rare) {
+    cudaEventRecord(e->ev_fork3, e->cur);
+    cudaStreamWaitEvent(e->side3, e->ev_fork3, 0);
+    e->cur = e->side3;
+  }
+  cond_begin(e, COND_RARE);
   LAUNCH(KC_RESOLVE, k_resolve_closure, 1, 1024, c);
   LAUNCH(KC_RESOLVE, k_resolve_comp, 148, 32 * RC_WARPS, c);
   LAUNCH(KC_RESOLVE, k_resolve, 1, 32, c);
@@ -328,8 +329,13 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
   LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
-  if (cond_else(e)) LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 0);
   cond_end(e);
+  if (fork_rare) {
+    cudaEventRecord(e->ev_join3, e->side3);
+    e->cur = main_s;
+  }
+  LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 0);
+  if (fork_rare) cudaStreamWaitEvent(e->cur, e->ev_join3, 0);
   if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
 }
 
@@ -582,39 +588,58 @@ static int ensure_windows(tsb_engine* e, int32_t n_steps) {
   return TSB_OK;
 }
 
-static int build_graph(tsb_engine* e) {
-  if (e->gexec) {
-    cudaGraphExecDestroy(e->gexec);
-    e->gexec = nullptr;
+// Captures `copies` consecutive steps into one graph (each copy with its own
+// conditional handle: kernel arguments are captured by value).
+static int capture_steps(tsb_engine* e, int copies, cudaGraph_t* graph, cudaGraphExec_t* exec, int* launches) {
+  if (*exec) {
+    cudaGraphExecDestroy(*exec);
+    *exec = nullptr;
   }
-  if (e->graph) {
-    cudaGraphDestroy(e->graph);
-    e->graph = nullptr;
+  if (*graph) {
+    cudaGraphDestroy(*graph);
+    *graph = nullptr;
   }
   CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-  {
-    cudaStreamCaptureStatus st;
-    unsigned long long id;
-    cudaGraph_t g;
-    const cudaGraphNode_t* deps;
-    size_t nd;
-    CK(cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd));
-    for (int k = 0; k < N_COND && !(e->c.debug & 8); k++)
-      CK(cudaGraphConditionalHandleCreate((cudaGraphConditionalHandle*)&e->c.cond[k], g, 0,
-                                          cudaGraphCondAssignDefault));
-  }
   e->c.use_cond = (e->c.debug & 8) ? 0 : 1;  // debug bit 3: gated kernels instead of IF nodes
   e->capturing = true;
   e->capture_err = cudaSuccess;
   Launcher L{e};
-  issue_step(e, L, 0);
+  for (int k = 0; k < copies; k++) {
+    if (e->c.use_cond) {
+      cudaStreamCaptureStatus st;
+      unsigned long long id;
+      cudaGraph_t g;
+      const cudaGraphNode_t* deps;
+      size_t nd;
+      cudaError_t er = cudaStreamGetCaptureInfo(e->stream, &st, &id, &g, &deps, &nd);
+      for (int q = 0; q < N_COND && er == cudaSuccess; q++)
+        er = cudaGraphConditionalHandleCreate((cudaGraphConditionalHandle*)&e->c.cond[q], g, 0,
+                                              cudaGraphCondAssignDefault);
+      if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
+    }
+    issue_step(e, L, 0);
+  }
   e->capturing = false;
   e->c.use_cond = 0;
   e->cur = e->stream;
+  cudaGraph_t g = nullptr;
+  const cudaError_t er = cudaStreamEndCapture(e->stream, &g);
   CK(e->capture_err);
-  CK(cudaStreamEndCapture(e->stream, &e->graph));
-  CK(cudaGraphInstantiate(&e->gexec, e->graph, 0));
-  e->launches_per_step = L.count;
+  CK(er);
+  *graph = g;
+  CK(cudaGraphInstantiate(exec, *graph, 0));
+  *launches = L.count / copies;
+  return TSB_OK;
+}
+
+// The step graph (one step) and the batch graph (STEPS_PER_BATCH steps: the
+// launch gap between graph replays, ~10 us, is paid once per batch).
+static constexpr int STEPS_PER_BATCH = 4;
+static int build_graph(tsb_engine* e) {
+  int n1 = 0, n4 = 0;
+  RC(capture_steps(e, 1, &e->graph, &e->gexec, &n1));
+  RC(capture_steps(e, STEPS_PER_BATCH, &e->graph4, &e->gexec4, &n4));
+  e->launches_per_step = n1;
   e->graph_dirty = false;
   return TSB_OK;
 }
@@ -643,7 +668,10 @@ static int do_steps(tsb_engine* e, int32_t n) {
     return TSB_OK;
   }
   if (e->graph_dirty) RC(build_graph(e));
-  for (int32_t k = 0; k < n; k++) CK(cudaGraphLaunch(e->gexec, e->stream));
+  int32_t k = 0;
+  if (!(e->c.debug & 32))
+    for (; k + STEPS_PER_BATCH <= n; k += STEPS_PER_BATCH) CK(cudaGraphLaunch(e->gexec4, e->stream));
+  for (; k < n; k++) CK(cudaGraphLaunch(e->gexec, e->stream));
   return TSB_OK;
 }
 
@@ -710,6 +738,9 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   CK(cudaStreamCreateWithFlags(&e->body, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->side3, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->ev_fork3, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join3, cudaEventDisableTiming));
   {
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1072,6 +1103,8 @@ void tsb_destroy(tsb_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  if (e->gexec4) cudaGraphExecDestroy(e->gexec4);
+  if (e->graph4) cudaGraphDestroy(e->graph4);
   if (e->graph) cudaGraphDestroy(e->graph);
   for (int q = 0; q < 2 * 96; q++)
     if (e->ev[q]) cudaEventDestroy(e->ev[q]);

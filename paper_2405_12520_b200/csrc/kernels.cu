@@ -96,6 +96,11 @@ enum { COND_RARE = 0, N_COND = 1 };
 __device__ __forceinline__ void set_cond(const Ctx& c, int k, bool v) {
   if (c.use_cond && v) cudaGraphSetConditional(c.cond[k], 1u);
 }
+// The step needs the RARE body of the step graph (engine.cu issue_step).
+__device__ __forceinline__ void set_rare(const Ctx& c) {
+  set_cond(c, COND_RARE, true);
+  c.dyn->rare = 1;
+}
 
 // A lane whose membership or order changed after the sweep; the next
 // snapshot rebuilds only these lanes (k_patch_*), unless too many changed.
@@ -1586,7 +1591,7 @@ static constexpr int RC_WARPS = 2;
 static constexpr int PATCH_MAX = 4096;  // dirty lanes (and moved vehicles) the patch handles
 __device__ void rare_if_unpatchable(const Ctx& c) {
   const Dyn* dy = c.dyn;
-  if (dy->n_dirty > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) set_cond(c, COND_RARE, true);
+  if (dy->n_dirty > PATCH_MAX || dy->n_moved > PATCH_MAX || (c.debug & 2)) set_rare(c);
 }
 
 // Fast-path replay on chip.  Every vehicle that can be on a closure lane
@@ -1789,7 +1794,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   }
   if (ne > RF_BLOCKS * RC_WARPS || (c.debug & 5)) {  // debug bit 0: sequential, bit 2: general path
     if (gtid() == 0) {
-      set_cond(c, COND_RARE, true);
+      set_rare(c);
       dy->n_resolve_general++;
     }
     return;
@@ -1888,7 +1893,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   __syncwarp();
   if (s_bad[w]) {
     if (ev == 0 && lid == 0) {
-      set_cond(c, COND_RARE, true);
+      set_rare(c);
       dy->n_resolve_general++;
     }
     return;
@@ -2127,7 +2132,7 @@ __global__ void k_inject_due(Ctx c) {
     dy->n_due = nr + nn;
     dy->n_retry = 0;
     dy->injected_now = 0;
-    set_cond(c, COND_RARE, nr + nn > 0);
+    if (nr + nn > 0) set_rare(c);
     if (nr + nn > 0) dy->n_inject_steps++;
   }
 }
@@ -2370,8 +2375,11 @@ __device__ void regroup_finish(const Ctx& c) {
 static constexpr int RG_BLOCKS = 296;
 __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) {
   PDL_WAIT();
-  TL_MARK(TL_REGROUP);
   Dyn* dy = c.dyn;
+  // two launches per step: the RARE body's (may_full) and the common one;
+  // exactly one of them works
+  if (may_full ? !dy->rare : dy->rare) return;
+  TL_MARK(TL_REGROUP);
   __shared__ int32_t sd[PATCH_MAX];
   __shared__ VRec sm[PD_WARPS][PD_CAP];
   __shared__ int s_last;
@@ -2508,6 +2516,7 @@ __global__ void k_begin_step(Ctx c) {
   dy->rf_done = 0;
   dy->rg_done = 0;
   dy->rf_fin = 0;
+  dy->rare = 0;
 }
 
 __global__ void k_zero_cnt(Ctx c, const int32_t* gate) {
