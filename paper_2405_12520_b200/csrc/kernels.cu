@@ -907,6 +907,30 @@ __global__ void k_place(Ctx c) {
     const bool st = valid && c.stay[j];
     const unsigned stay_bits = __ballot_sync(0xffffffffu, st);
     const int32_t L = r.lane;
+    // stayer rank in its lane = stayers ahead of it in its snapshot range
+    // [a0, j): inside the warp from the ballot; before the warp only for the
+    // lane whose range covers `base` -- the first stayer's lane, if its range
+    // starts before the warp -- counted by the whole warp, 32 at a time
+    const int32_t a0 = st ? seg(c, SA, L).x : 0;
+    const int first_st = stay_bits ? __ffs(stay_bits) - 1 : 0;
+    const int32_t Ls = __shfl_sync(0xffffffffu, L, first_st);
+    const int32_t a0s = __shfl_sync(0xffffffffu, a0, first_st);
+    int32_t before = 0, kb = -1;  // its stayers in [a0s, base), the last of them
+    if (stay_bits && a0s < base) {
+      for (int32_t hi = base; hi > a0s; hi -= 32) {
+        const int32_t q = hi - 1 - lid;
+        const unsigned bq = __ballot_sync(0xffffffffu, q >= a0s && c.stay[q]);
+        if (kb < 0 && bq) kb = hi - __ffs(bq);  // nearest first: lowest lid = largest q
+        before += __popc(bq);
+      }
+    }
+    const unsigned below = (1u << lid) - 1u;
+    const int lo_lane = a0 > base ? a0 - base : 0;
+    const unsigned prev_bits = stay_bits & below & ~((1u << lo_lane) - 1u);
+    // previous stayer inside the warp: its record by shuffle
+    const int pl = prev_bits ? 31 - __clz(prev_bits) : lid;
+    const double pr_s = __shfl_sync(0xffffffffu, r.s, pl);
+    const int32_t pr_vix = __shfl_sync(0xffffffffu, r.vix, pl);
     bool flag = false;  // this lane needs k_lanefix
     if (L >= 0) {
       if (!st) {
@@ -914,27 +938,23 @@ __global__ void k_place(Ctx c) {
         C[pos] = r;
         flag = true;
       } else {
-        // rank among the lane's stayers: stayers ahead of j in its snapshot
-        // segment [a0, j) -- inside this warp from the ballot, before it by a
-        // short loop (only for the warp's first segment)
-        const int32_t a0 = seg(c, SA, L).x;
-        const int lo_lane = a0 > base ? a0 - base : 0;
-        const unsigned below = (1u << lid) - 1u, from = ~((1u << lo_lane) - 1u);
-        int32_t rank = __popc(stay_bits & below & from);
-        int32_t k = -1;  // previous stayer
-        const unsigned prev_bits = stay_bits & below & from;
-        if (prev_bits) k = base + 31 - __clz(prev_bits);
-        for (int32_t q = base - 1; q >= a0; q--) {
-          if (c.stay[q]) {
-            rank++;
-            if (k < 0) k = q;
-          }
-        }
+        const bool straddle = a0 < base;  // then L == Ls
+        const int32_t rank = __popc(prev_bits) + (straddle ? before : 0);
         C[CS[L] + rank] = r;
-        if (k >= 0) {
-          const VRec pr = c.B[k];
-          flag = !ahead_of(pr.s, pr.vix, r.s, r.vix) || r.s > ((pr.s - p.L) - p.s0_floor) + 1e-12;
+        double ps;
+        int32_t pv;
+        bool have = true;
+        if (prev_bits) {
+          ps = pr_s;
+          pv = pr_vix;
+        } else if (straddle && kb >= 0) {
+          const VRec pr = c.B[kb];
+          ps = pr.s;
+          pv = pr.vix;
+        } else {
+          have = false;
         }
+        if (have) flag = !ahead_of(ps, pv, r.s, r.vix) || r.s > ((ps - p.L) - p.s0_floor) + 1e-12;
       }
     }
     // warp-aggregated append of newly flagged lanes: one flag atomic per lane
