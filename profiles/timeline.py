@@ -19,6 +19,8 @@ PH = ["begin", "update", "scan", "place", "lanefix", "resolve_fast", "regroup", 
       "inject_due"]
 net, flat, trips, ft = bench.build_workload(1_000_000, 29.0)
 w = World.from_flat(flat, ft, EngineConfig(), seed=42, pow_mode=0)
+if os.environ.get("TSB_DEBUG"):
+    _native.check(_native.lib().tsb_set_debug(w._h, int(os.environ["TSB_DEBUG"])))
 w.step()
 w.run(20)
 w.run(40)
