@@ -8,6 +8,6 @@ for v in "$@"; do
   set -- $v
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
     -Xcompiler -fPIC,-ffp-contract=off,-O2 -Xptxas -v -DUPD_BT=$1 -DUPD_MINB=$2 -shared \
-    -o ../../build_variants/lib_$1_$2.so engine.cu router.cpp 2>&1 | grep -A2 "k_updateENS" | grep -E "spill|registers" | tr '\n' ' '
+    -o ../../build_variants/lib_$1_$2.so engine.cu router.cpp 2>&1 | grep -A2 "k_updateILb0" | grep -E "spill|registers" | tr '\n' ' '
   echo "-> lib_$1_$2.so"
 done
