@@ -271,7 +271,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--vehicles", type=int, default=1_000_000)
     ap.add_argument("--spacing", type=float, default=29.0)
-    ap.add_argument("--cpu-sample-steps", type=int, default=6)
+    ap.add_argument("--cpu-sample-steps", type=int, default=3)
+    ap.add_argument("--cpu-warm-steps", type=int, default=11)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--debug", type=int, default=0, help="tsb_set_debug flags (experiments; results unchanged)")
     ap.add_argument("--pow", default="correct", choices=["correct", "glibc"],
@@ -291,16 +292,18 @@ def main():
         if rank != 0:
             return
         net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
-        k = max(1, min(args.steps, 10))
+        k = max(1, min(args.steps, args.cpu_sample_steps))
         cores = os.cpu_count() or 1
-        rate, u, dt = cpu_baseline(net, flat, trips, min(args.warmup, 3), k, cores)
+        rate, u, dt = cpu_baseline(net, flat, trips, args.cpu_warm_steps, k, cores)
         line = {
             "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": n_gpus,
-            "steps": k, "warmup": min(args.warmup, 3), "ms_per_step": 1000.0 * dt / k,
+            "steps": k, "warmup": args.cpu_warm_steps, "ms_per_step": 1000.0 * dt / k,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload, "parallelism": f"cpu-{cores}-threads"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{k} steps x {args.vehicles} vehicles after injection + warm-up; "
+                             "sample": f"{k} steps x {args.vehicles} vehicles after injection + "
+                                       f"{args.cpu_warm_steps} warm-up steps (the revert regime the GPU arm is "
+                                       "timed in); "
                                        "oracle/oracle.c (C restatement of trafficsim World.step; the "
                                        f"reference is pure Python and cannot travel), update phase on {cores} "
                                        "threads, commit phase sequential as in the reference"},
@@ -390,10 +393,12 @@ def main():
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        rate, u, dt = cpu_baseline(net, flat, trips, 1, args.cpu_sample_steps, cores)
+        rate, u, dt = cpu_baseline(net, flat, trips, args.cpu_warm_steps, args.cpu_sample_steps, cores)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{args.cpu_sample_steps} steps x {n_drv} vehicles of the same M1 workload after "
-                         "injection + 1 warm-up step; oracle/oracle.c (C restatement of World.step), update "
+                         f"injection + {args.cpu_warm_steps} warm-up steps (the revert regime the GPU arm is "
+                         "timed in: the reference restarts its sweep after every revert); "
+                         "oracle/oracle.c (C restatement of World.step), update "
                          f"phase on {cores} threads, commit phase sequential as in the reference"}
     if rank != 0:
         return

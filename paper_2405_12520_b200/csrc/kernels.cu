@@ -2492,7 +2492,8 @@ __global__ void k_speeds(Ctx c, int flush) {
     int32_t cnt = 0;
     for (int32_t L = span.x; L <= span.y; L++) {
       const int2 sg = seg(c, S, L);
-      for (int32_t j = sg.x; j < sg.y; j++) sum += __ldg(&A[j].v);
+#pragma unroll 8
+      for (int32_t j = sg.x; j < sg.y; j++) sum += __ldg(&A[j].v);  // loads issued ahead, adds in order
       cnt += sg.y - sg.x;
     }
     if (cnt == 0) continue;
