@@ -899,8 +899,12 @@ __global__ void k_place(Ctx c) {
   }
   const int32_t n = dy->n_a + (c.sharded ? dy->n_g : 0);
   const int lid = threadIdx.x & 31;
-  // one pass, whole warps (the ballots below need all 32 lanes)
-  for (int32_t base = (gtid() >> 5) << 5; base < n; base += gstride()) {
+  __shared__ int32_t s_cnt, s_base;
+  __shared__ int32_t s_list[256];
+  // one pass in the usual case; block-uniform trip count (the block-level
+  // append below synchronises), whole warps (the ballots need all 32 lanes)
+  for (int32_t bbase = blockIdx.x * blockDim.x; bbase < n; bbase += gstride()) {
+    const int32_t base = bbase + (threadIdx.x & ~31);
     const int32_t j = base + lid;
     const bool valid = j < n;
     const VRec r = valid ? c.B[j] : VRec{0.0, 0.0, 0, 0, -1, 0};
@@ -957,22 +961,25 @@ __global__ void k_place(Ctx c) {
         if (have) flag = !ahead_of(ps, pv, r.s, r.vix) || r.s > ((ps - p.L) - p.s0_floor) + 1e-12;
       }
     }
-    // warp-aggregated append of newly flagged lanes: one flag atomic per lane
-    // per warp (jammed lanes flag every vehicle), one counter atomic per warp
+    // append newly flagged lanes: one flag atomic per lane per warp (jammed
+    // lanes flag every vehicle), collected per block in shared memory, one
+    // counter atomic per block (a per-warp counter atomic serialised ~30k
+    // same-address atomics per step)
     const unsigned fm = __ballot_sync(0xffffffffu, flag);
     bool first_flag = false;
     if (flag) {
       const unsigned grp = __match_any_sync(fm, L);
       if (lid == __ffs(grp) - 1) first_flag = atomicExch(&c.fix_flag[L], 1) == 0;
     }
-    const unsigned fb = __ballot_sync(0xffffffffu, first_flag);
-    if (fb) {
-      int32_t slot0 = 0;
-      const int leader = __ffs(fb) - 1;
-      if (lid == leader) slot0 = atomicAdd(&dy->n_fix, __popc(fb));
-      slot0 = __shfl_sync(0xffffffffu, slot0, leader);
-      if (first_flag) c.fix_list[slot0 + __popc(fb & ((1u << lid) - 1))] = L;
-    }
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    if (first_flag) s_list[atomicAdd(&s_cnt, 1)] = L;
+    __syncthreads();
+    const int32_t nb = s_cnt;
+    if (threadIdx.x == 0 && nb) s_base = atomicAdd(&dy->n_fix, nb);
+    __syncthreads();
+    for (int32_t k = threadIdx.x; k < nb; k += blockDim.x) c.fix_list[s_base + k] = s_list[k];
+    __syncthreads();
   }
 }
 
