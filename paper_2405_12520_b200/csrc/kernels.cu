@@ -990,6 +990,8 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   TL_MARK(TL_LANEFIX);
   __shared__ VRec s_in[LX_WARPS][LX_CAP];
   __shared__ VRec s_out[LX_WARPS][LX_CAP];
+  __shared__ double s_snap_s[LX_WARPS][LX_CAP];
+  __shared__ int32_t s_snap_l[LX_WARPS][LX_CAP];
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
@@ -1028,19 +1030,40 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    // the sweep reads each member's snapshot lane / s: gathered in parallel
+    // first (on-chip lanes), not one dependent load per member in lane 0
+    const bool pre = on_chip && first < n;
+    if (pre) {
+      for (int32_t q = first - 1 + lid; q < n; q += 32) {
+        const VRec sn = A[out[q].src];
+        s_snap_l[w][q] = sn.lane;
+        s_snap_s[w][q] = sn.s;
+      }
+      __syncwarp();
+    }
+    int32_t q_ev = -1;  // event: members [first, q_ev) were clamped and are restored
     if (first < n && lid == 0) {
       VRec prev = out[first - 1];
-      bool prev_entered = prev.lane != A[prev.src].lane;
+      bool prev_entered = prev.lane != (pre ? s_snap_l[w][first - 1] : A[prev.src].lane);
       double prev_rear = prev.s - p.L;
       bool event = false;
       int32_t q = first;
       for (; q < n; q++) {
         VRec r = out[q];
         const double limit = prev_rear - p.s0_floor;
-        const VRec sn = A[r.src];
-        const bool entered = r.lane != sn.lane;
+        int32_t sn_lane;
+        double sn_s;
+        if (pre) {
+          sn_lane = s_snap_l[w][q];
+          sn_s = s_snap_s[w][q];
+        } else {
+          const VRec sn = A[r.src];
+          sn_lane = sn.lane;
+          sn_s = sn.s;
+        }
+        const bool entered = r.lane != sn_lane;
         if (r.s > limit + 1e-12) {
-          const double floor_s = entered ? 0.0 : sn.s;
+          const double floor_s = entered ? 0.0 : sn_s;
           if (limit >= floor_s) {
             r.v = py_max(0.0, py_min(r.v, r.v - (r.s - limit) / p.dt));
             r.s = limit;
@@ -1058,12 +1081,7 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
         prev_rear = r.s - p.L;
       }
       if (event) {
-        // leave the lane unswept (post-delta values) for the replay
-        for (int32_t u = first; u < q; u++) {
-          const VRec o = c.B[out[u].src];
-          out[u].s = o.s;
-          out[u].v = o.v;
-        }
+        q_ev = q;
         c.events[atomicAdd(&dy->n_events, 1)] = L;
       } else {
         // a hold can break the (s desc) order; the next snapshot must be re-sorted
@@ -1072,6 +1090,16 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
             mark_dirty(c, L);
             break;
           }
+      }
+    }
+    q_ev = __shfl_sync(0xffffffffu, q_ev, 0);
+    __syncwarp();
+    if (q_ev >= 0) {
+      // leave the lane unswept (post-delta values) for the replay
+      for (int32_t u = first + lid; u < q_ev; u += 32) {
+        const VRec o = c.B[out[u].src];
+        out[u].s = o.s;
+        out[u].v = o.v;
       }
     }
     __syncwarp();
