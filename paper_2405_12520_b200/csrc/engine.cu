@@ -42,7 +42,10 @@ static int fail(int code, const char* fmt, ...) {
     if (_r) return _r;     \
   } while (0)
 
-static const int SCAN_BT = 256, SCAN_IPT = 8, SCAN_TILE = SCAN_BT * SCAN_IPT;
+#ifndef SCAN_IPT_CFG
+#define SCAN_IPT_CFG 8
+#endif
+static const int SCAN_BT = 256, SCAN_IPT = SCAN_IPT_CFG, SCAN_TILE = SCAN_BT * SCAN_IPT;
 
 enum KernelClass {
   KC_UPDATE,
