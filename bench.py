@@ -73,8 +73,9 @@ def run_sharded(args, ws, rank, local, pg, workload):
 
     net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
     jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    p2p = args.exchange == "p2p"
     sw = ShardedWorld(flat, ft, jp, EngineConfig(), 42, rank, ws, device=local,
-                      host_staging=os.environ.get("TSB_BENCH_GLOO") == "1")
+                      host_staging=os.environ.get("TSB_BENCH_GLOO") == "1", p2p=p2p)
     L = _native.lib()
     sw.step_local(1)  # bulk injection (excluded)
     with ClockSampler(local) as clk:
@@ -116,7 +117,10 @@ def run_sharded(args, ws, rank, local, pg, workload):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "vehicles_total": args.vehicles, "lanes": flat.n_lanes,
                    "parallelism": f"lane bands x{ws} (sharded.py; halo lanes rank0: {halo} vs own {own})",
-                   "exchange": "per step: NCCL all_to_all_single of boundary-lane packets + counters",
+                   "exchange": ("per step: pack kernel writes boundary-lane packets into the peers' "
+                                "IPC-mapped receive slots (NVLink P2P), release/acquire flags, ghost import; "
+                                "no host synchronisation" if p2p else
+                                "per step: NCCL all_to_all_single of boundary-lane packets + counters"),
                    "exchanged_bytes_rank0_total": xbytes,
                    "timing": "engine-stream events around K steps incl. exchanges, max over ranks"},
         "e2e": {"value": (u2 - u1) / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -275,6 +279,8 @@ def main():
     ap.add_argument("--cpu-warm-steps", type=int, default=11)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--debug", type=int, default=0, help="tsb_set_debug flags (experiments; results unchanged)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: device-driven exchange over peer memory, or NCCL all-to-all")
     ap.add_argument("--pow", default="correct", choices=["correct", "glibc"],
                     help="IDM power arithmetic of the headline run: correctly rounded (within the "
                          "north-star tolerance of the reference) or glibc pow (bit-identical to the "

@@ -136,8 +136,29 @@ int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes);
  * messages concatenated in rank order, bytes[q] each). */
 int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes);
 
+/* Device-driven exchange over peer memory (replaces export + the host's
+ * all-to-all + import; NVLink P2P between GPUs, CUDA IPC between processes):
+ * tsb_shard_p2p_alloc returns this rank's receive slots (2 x nranks slots of
+ * *slot_bytes) and arrival flags (2 x nranks u64), both cudaMalloc bases, so
+ * tsb_ipc_handle can export them; every rank opens its peers' with
+ * tsb_ipc_open and passes them (rank order, own entry ignored) to
+ * tsb_shard_p2p_set_peers.  tsb_shard_p2p_exchange then enqueues, on the
+ * engine stream and without a host synchronisation, the pack written
+ * straight into each peer's slot, a release of the peer's flag, the wait
+ * for every peer's flag and the ghost import. */
+int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes);
+int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags);
+int tsb_shard_p2p_exchange(tsb_engine* e);
+/* cudaIpcGetMemHandle / cudaIpcOpenMemHandle (64-byte handles). */
+#define TSB_IPC_HANDLE_BYTES 64
+int tsb_ipc_handle(const void* dev_ptr, uint8_t* handle);
+int tsb_ipc_open(const uint8_t* handle, void** dev_ptr);
+
 /* World.step() x n (world.py:659-689); report of the last step (may be NULL). */
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last);
+/* tsb_step without the final synchronisation (errors surface at the next
+ * synchronising call); for pipelines such as the sharded P2P loop. */
+int tsb_step_async(tsb_engine* e, int32_t n_steps);
 /* Current counters without stepping. */
 int tsb_report_get(tsb_engine* e, tsb_report* out);
 

@@ -54,6 +54,12 @@ SIGNATURES = {
     "tsb_marks_elapsed": (_i32, [_vp, _i32, _i32, C.POINTER(_f64)]),
     "tsb_shard_export": (_i32, [_vp, _vp, _i64, _vp]),
     "tsb_shard_import": (_i32, [_vp, _vp, _vp]),
+    "tsb_shard_p2p_alloc": (_i32, [_vp, _vp, _vp, _vp]),
+    "tsb_shard_p2p_set_peers": (_i32, [_vp, _vp, _vp]),
+    "tsb_shard_p2p_exchange": (_i32, [_vp]),
+    "tsb_step_async": (_i32, [_vp, _i32]),
+    "tsb_ipc_handle": (_i32, [_vp, _vp]),
+    "tsb_ipc_open": (_i32, [_vp, _vp]),
 }
 
 _lib = None

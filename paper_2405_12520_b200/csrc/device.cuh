@@ -209,6 +209,12 @@ struct Ctx {
   int32_t* imp_pos;
   int64_t peer_first_exp[9], peer_first_imp[9];  // entry index ranges per peer (nranks <= 8)
   int32_t nranks, rank;
+  // device-driven exchange over peer memory (tsb_shard_p2p_*): each rank's
+  // receive slots [parity][source rank] and arrival flags, mapped in every peer
+  uint8_t* p2p_peer_recv[8];
+  unsigned long long* p2p_peer_flag[8];
+  unsigned long long* p2p_flag;  // own flags [parity][source rank]
+  int64_t p2p_slot;               // bytes per slot
   int32_t* comp_flags;  // per component: bit 0 has an own lane, bit 1 has an inexact lane
   // conditional sections of the step graph (kernels.cu set_cond)
   unsigned long long cond[4];

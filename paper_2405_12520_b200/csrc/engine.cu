@@ -101,6 +101,8 @@ struct tsb_engine {
   cudaStream_t side3 = nullptr;  // parallel branch (the RARE body's IF node)
   cudaStream_t cond_on = nullptr;  // stream a conditional node is being captured on
   cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
+  uint8_t* p2p_recv = nullptr;        // own receive slots (device-driven exchange)
+  unsigned long long p2p_epoch = 0;   // exchanges so far
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
@@ -1102,6 +1104,84 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes) {
   return TSB_OK;
 }
 
+// ---- device-driven exchange over peer memory (kernels.cu k_exp_pack_p2p)
+
+int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes) {
+  if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
+  Ctx& c = e->c;
+  CK(cudaSetDevice(e->device));
+  if (!c.p2p_flag) {
+    // a slot holds one peer's message: per-lane counts (<= every lane) + records (<= every vehicle)
+    c.p2p_slot = (((int64_t)4 * e->n_lanes + 31) & ~(int64_t)31) + (int64_t)32 * std::max(e->n_trips, 1) + 64;
+    uint8_t* r = nullptr;
+    unsigned long long* f = nullptr;
+    CK(cudaMalloc((void**)&r, (size_t)(2 * c.nranks) * (size_t)c.p2p_slot));
+    e->allocs.push_back(r);
+    CK(cudaMalloc((void**)&f, sizeof(unsigned long long) * 2 * c.nranks));
+    e->allocs.push_back(f);
+    CK(cudaMemset(f, 0, sizeof(unsigned long long) * 2 * c.nranks));
+    e->p2p_recv = r;
+    c.p2p_flag = f;
+  }
+  *recv = e->p2p_recv;
+  *flags = c.p2p_flag;
+  *slot_bytes = c.p2p_slot;
+  return TSB_OK;
+}
+
+int tsb_ipc_handle(const void* dev_ptr, uint8_t* handle) {
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &h, sizeof(h));
+  return TSB_OK;
+}
+
+int tsb_ipc_open(const uint8_t* handle, void** dev_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TSB_OK;
+}
+
+int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags) {
+  if (!e || !e->c.sharded || !e->c.p2p_flag) return fail(TSB_EINVAL, "call tsb_shard_p2p_alloc first");
+  Ctx& c = e->c;
+  if (c.nranks > 8) return fail(TSB_EINVAL, "at most 8 ranks");
+  for (int q = 0; q < c.nranks; q++) {
+    c.p2p_peer_recv[q] = (uint8_t*)peer_recv[q];
+    c.p2p_peer_flag[q] = (unsigned long long*)peer_flags[q];
+  }
+  e->graph_dirty = true;  // Ctx is captured by value
+  return TSB_OK;
+}
+
+int tsb_shard_p2p_exchange(tsb_engine* e) {
+  if (!e || !e->c.sharded || !e->c.p2p_flag) return fail(TSB_EINVAL, "P2P exchange not set up");
+  Ctx& c = e->c;
+  const unsigned long long epoch = ++e->p2p_epoch;
+  cudaStream_t st = e->stream;
+  if (c.n_exp > 0) {
+    k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, st>>>(c);
+    const int ntiles = c.n_exp / SCAN_TILE + 1;
+    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, st>>>(c, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE, nullptr,
+                                                            c.n_exp, ntiles, nullptr);
+    k_exp_pack_p2p<<<grid_for((int64_t)c.n_exp * 32, 256, 1 << 20), 256, 0, st>>>(c, epoch);
+  }
+  k_p2p_signal<<<1, 32, 0, st>>>(c, epoch);
+  k_p2p_wait<<<1, 32, 0, st>>>(c, epoch);
+  if (c.n_imp > 0) {
+    SrcBase sb{};
+    for (int q = 0; q < c.nranks; q++) sb.b[q] = (int64_t)((epoch & 1) * c.nranks + q) * c.p2p_slot;
+    k_imp_count<<<grid_for(c.n_imp, 256, 1 << 20), 256, 0, st>>>(c, e->p2p_recv, sb);
+    const int ntiles = c.n_imp / SCAN_TILE + 1;
+    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, st>>>(c, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE, nullptr,
+                                                            c.n_imp, ntiles, nullptr);
+    k_imp_copy<<<grid_for((int64_t)c.n_imp * 32, 256, 1 << 20), 256, 0, st>>>(c, e->p2p_recv, sb);
+  }
+  CK(cudaGetLastError());
+  return TSB_OK;  // no host synchronisation: the next step follows in stream order
+}
+
 void tsb_destroy(tsb_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
@@ -1149,6 +1229,15 @@ int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last) {
   RC(do_steps(e, n_steps));
   RC(sync_dyn(e));
   if (last) fill_report(e, last);
+  return TSB_OK;
+}
+
+int tsb_step_async(tsb_engine* e, int32_t n_steps) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  if (n_steps < 0) return fail(TSB_EINVAL, "steps must be non-negative");
+  if (e->n_closed > 0) return tsb_step(e, n_steps, nullptr);  // host continuation needs the syncs
+  CK(cudaSetDevice(e->device));
+  RC(do_steps(e, n_steps));
   return TSB_OK;
 }
 

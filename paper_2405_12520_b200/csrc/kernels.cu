@@ -2676,6 +2676,59 @@ __global__ void k_exp_pack(Ctx c, uint8_t* send) {
   }
 }
 
+// Device-driven exchange over peer memory (NVLink P2P / CUDA IPC): the pack
+// writes each peer's message straight into that peer's receive slot for this
+// rank and step parity -- the same layout as k_exp_pack's -- then
+// k_p2p_signal publishes the step epoch in the peer's flag for this rank and
+// k_p2p_wait waits for every peer's flag before the import reads the local
+// slots.  Two slot sets by step parity: a rank writes parity t+1 only after
+// its own import of step t saw every peer's step-t flag, which each peer
+// raised after importing step t-1 from that slot set.
+__global__ void k_exp_pack_p2p(Ctx c, unsigned long long epoch) {
+  PDL_WAIT();
+  const VRec* A = c.lay[c.dyn->cur];
+  const int2* S = c.rng[c.dyn->cur];
+  const int lid = threadIdx.x & 31;
+  const int64_t slot = (int64_t)((epoch & 1) * c.nranks + c.rank) * c.p2p_slot;
+  for (int32_t e = gtid() >> 5; e < c.n_exp; e += gstride() >> 5) {
+    const int q = c.exp_peer[e];
+    const int64_t e0 = c.peer_first_exp[q];
+    uint8_t* base = c.p2p_peer_recv[q] + slot;
+    const int32_t L = c.exp_lane[e];
+    const int32_t n = c.exp_cnt[e];
+    if (lid == 0) ((int32_t*)base)[e - e0] = n;
+    VRec* dst = (VRec*)(base + align32(4 * (c.peer_first_exp[q + 1] - e0))) + (c.exp_pos[e] - c.exp_pos[e0]);
+    const int32_t at = seg(c, S, L).x;
+    for (int32_t k = lid; k < n; k += 32) dst[k] = A[at + k];
+  }
+}
+
+__global__ void k_p2p_signal(Ctx c, unsigned long long epoch) {
+  PDL_WAIT();
+  __threadfence_system();  // the pack's remote writes before the flags
+  const int q = threadIdx.x;
+  if (q < c.nranks && q != c.rank) {
+    unsigned long long* f = c.p2p_peer_flag[q] + (epoch & 1) * c.nranks + c.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+}
+
+__global__ void k_p2p_wait(Ctx c, unsigned long long epoch) {
+  PDL_WAIT();
+  const int q = threadIdx.x;
+  if (q < c.nranks && q != c.rank) {
+    const unsigned long long* f = c.p2p_flag + (epoch & 1) * c.nranks + q;
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
 // Receive side: counts from the headers (src_base[q] = byte offset of
 // source q's message in the receive buffer).
 struct SrcBase {
@@ -2705,6 +2758,10 @@ __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
     const VRec* src = (const VRec*)(recv + sb.b[q] + align32(4 * (c.peer_first_imp[q + 1] - e0))) +
                       (c.imp_pos[e] - c.imp_pos[e0]);
     const int32_t at = base + c.imp_pos[e];
+    if ((int64_t)at + n > c.cap_rec) {  // ghost capacity (fails loudly at the next sync)
+      if (lid == 0) dy->overflow |= 64;
+      continue;
+    }
     if (lid == 0) c.rng[dy->cur][L] = make_int2(at, at + n);
     for (int32_t k = lid; k < n; k += 32) A[at + k] = src[k];
   }

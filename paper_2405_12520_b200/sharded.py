@@ -11,10 +11,16 @@ One step on rank r is
    revert partners); chains that would leave the exactly-computed zone make
    the engine fail loudly (TSB_ECAP), never silently diverge;
 2. one exchange: each rank packs the vehicles of its own lanes that lie in a
-   peer's halo (tsb_shard_export, device buffers) and the peers' packets
-   become its ghosts for the next step (tsb_shard_import).  The transfer is
-   `torch.distributed.all_to_all_single` on device tensors -- NCCL over
-   NVLink/NVSwitch on a multi-GPU node; gloo with host staging for tests;
+   peer's halo and the peers' packets become its ghosts for the next step.
+   Two transports:
+   * p2p=True (device-driven): the pack kernel writes each message straight
+     into the peer's receive slot (peer memory mapped with CUDA IPC; NVLink
+     P2P between GPUs), releases the peer's arrival flag, waits for its own
+     flags and imports -- all enqueued on the engine stream, no host
+     synchronisation and no collective per step (tsb_shard_p2p_*);
+   * otherwise tsb_shard_export / tsb_shard_import around
+     `torch.distributed.all_to_all_single` on device tensors (NCCL), or gloo
+     with host staging;
 3. step counters (driving, waiting, finished, ...) are summed over ranks.
 
 Vehicles migrate implicitly: a vehicle that crosses into a peer's band was a
@@ -69,7 +75,7 @@ class ShardedWorld:
 
     def __init__(self, flat: FlatNet, ft: FlatTrips, junc_pos: np.ndarray, config: EngineConfig | None,
                  seed: int, rank: int, nranks: int, device: int = 0, group=None, host_staging: bool = False,
-                 pow_mode: int = 1):
+                 pow_mode: int = 1, p2p: bool = False):
         import torch
         import torch.distributed as dist
 
@@ -98,16 +104,42 @@ class ShardedWorld:
         self._recv = torch.zeros(len(ft.ids) * RECORD_BYTES + 4 * n_imp + 32 * nranks + 64, dtype=torch.uint8,
                                  device=self.device)
         self.exchanged_bytes = 0
+        self.p2p = p2p
+        if p2p:
+            self._setup_p2p()
         self._exchange()  # initial ghosts (empty network: zero vehicles)
+
+    def _setup_p2p(self):
+        """Receive slots and arrival flags of every rank mapped into every
+        other rank (CUDA IPC handles exchanged once through the process group)."""
+        L = _native.lib()
+        recv, flags, slot = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _native.check(L.tsb_shard_p2p_alloc(self._h, C.byref(recv), C.byref(flags), C.byref(slot)))
+        hr, hf = (C.c_uint8 * 64)(), (C.c_uint8 * 64)()
+        _native.check(L.tsb_ipc_handle(recv, hr))
+        _native.check(L.tsb_ipc_handle(flags, hf))
+        got = [None] * self.nranks
+        self.dist.all_gather_object(got, (bytes(hr), bytes(hf)), group=self.group)
+        pr, pf = (C.c_void_p * self.nranks)(), (C.c_void_p * self.nranks)()
+        for q, (br, bf) in enumerate(got):
+            if q == self.rank:
+                pr[q], pf[q] = recv, flags
+                continue
+            a, b = C.c_void_p(), C.c_void_p()
+            _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(br), C.byref(a)))
+            _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(bf), C.byref(b)))
+            pr[q], pf[q] = a, b
+        _native.check(L.tsb_shard_p2p_set_peers(self._h, pr, pf))
+        self.dist.barrier(group=self.group)  # every rank mapped before the first exchange
 
     @classmethod
     def from_network(cls, net, trips, config=None, seed=0, rank=0, nranks=1, device=0, group=None,
-                     host_staging=False):
+                     host_staging=False, p2p=False):
         config = config or EngineConfig()
         flat = flatten_network(net, config.controller)
         ft = flatten_trips(flat, trips)
         jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64).reshape(-1, 2)
-        return cls(flat, ft, jp, config, seed, rank, nranks, device, group, host_staging)
+        return cls(flat, ft, jp, config, seed, rank, nranks, device, group, host_staging, p2p=p2p)
 
     def close(self):
         if self._h is not None:
@@ -119,6 +151,9 @@ class ShardedWorld:
     # ------------------------------------------------------------ exchange
 
     def _exchange(self):
+        if self.p2p:
+            _native.check(_native.lib().tsb_shard_p2p_exchange(self._h))
+            return
         torch = self.torch
         out_b = np.zeros(self.nranks, dtype=np.int64)
         _native.check(_native.lib().tsb_shard_export(self._h, C.c_void_p(self._send.data_ptr()),
@@ -133,8 +168,13 @@ class ShardedWorld:
     def step_local(self, n: int = 1):
         """n steps, exchanging ghosts after each (no global reductions)."""
         for _ in range(n):
-            _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
+            if self.p2p:  # all on the engine stream: no host synchronisation per step
+                _native.check(_native.lib().tsb_step_async(self._h, 1))
+            else:
+                _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
             self._exchange()
+        if self.p2p:
+            _native.check(_native.lib().tsb_report_get(self._h, C.byref(self._report)))
 
     def report(self) -> dict:
         """StepReport counters summed over ranks (time and step are shared)."""

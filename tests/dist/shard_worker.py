@@ -3,7 +3,8 @@ engine, compared step by step with a single-GPU engine on the same inputs.
 
 Run: python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1
      --master-port P tests/dist/shard_worker.py SCENARIO STEPS
-All ranks may share one GPU (gloo exchange with host staging).
+All ranks may share one GPU (gloo exchange with host staging; with a third
+argument "p2p" the device-driven exchange over CUDA IPC-mapped peer memory).
 """
 
 from __future__ import annotations
@@ -28,12 +29,14 @@ SCEN = {
 
 def main():
     name, steps = sys.argv[1], int(sys.argv[2])
+    p2p = len(sys.argv) > 3 and sys.argv[3] == "p2p"
     dist.init_process_group("gloo")
     rank, ws = dist.get_rank(), dist.get_world_size()
     net, n, seed, window = SCEN[name]()
     trips = random_trips(net, n, seed=seed, window=window)
     cfg = EngineConfig()
-    sw = ShardedWorld.from_network(net, trips, cfg, seed=seed, rank=rank, nranks=ws, device=0, host_staging=True)
+    sw = ShardedWorld.from_network(net, trips, cfg, seed=seed, rank=rank, nranks=ws, device=0, host_staging=True,
+                                   p2p=p2p)
     ref = World(net, trips, cfg, seed=seed)
     own_zone = sw.plan.zone
     bad = 0
@@ -65,7 +68,8 @@ def main():
     t = torch.tensor(flag)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"SHARD_RESULT {name} ranks={ws} steps={steps} mismatches={int(t.item())} bytes_rank0={ex}", flush=True)
+        print(f"SHARD_RESULT {name} ranks={ws} steps={steps} p2p={int(p2p)} mismatches={int(t.item())} "
+              f"bytes_rank0={ex}", flush=True)
     dist.destroy_process_group()
 
 
