@@ -252,6 +252,10 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #ifndef UPD_GRID_CAP
 #define UPD_GRID_CAP (1 << 30)
 #endif
+#ifndef MOBIL_UNROLL
+#define MOBIL_UNROLL 2
+#endif
+static constexpr int kMobilUnroll = MOBIL_UNROLL;  // the two MOBIL sides: unrolled (ILP) or looped (code size)
 template <bool G>
 __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   PDL_WAIT();
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         // both sides evaluated without branches (a side that does not exist
         // or fails a check is evaluated on safe stand-ins and discarded):
         // the warp stays converged through the fp64 work
-#pragma unroll
+#pragma unroll(kMobilUnroll)
         for (int k = 0; k < 2; k++) {
           const int32_t nb = k < nsides ? sides[k] : -1;
           const int32_t nbs = nb >= 0 ? nb : snap_lane;
