@@ -50,8 +50,8 @@ static const int SCAN_BT = 256, SCAN_IPT = SCAN_IPT_CFG, SCAN_TILE = SCAN_BT * S
 enum KernelClass {
   KC_UPDATE,
   KC_SCAN,
-  KC_SCATTER,
-  KC_LANESORT_SWEEP,
+  KC_PLACE,
+  KC_LANEFIX,
   KC_RESOLVE,
   KC_SIGNALS,
   KC_INJECT,
@@ -60,7 +60,7 @@ enum KernelClass {
   KC_MISC,
   KC_COUNT
 };
-static const char* kKernelNames[KC_COUNT] = {"k_update",  "k_scan",   "k_scatter", "k_lanesort_sweep", "k_resolve",
+static const char* kKernelNames[KC_COUNT] = {"k_update",  "k_scan",   "k_place", "k_lanefix", "k_resolve",
                                              "k_signals", "k_inject", "k_regroup", "k_speeds",         "k_misc"};
 
 struct tsb_engine {
@@ -267,8 +267,8 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
   // bucket the post-delta state by lane, sort each lane, tentative sweep
   scan(e, L, KC_SCAN, SCAN_LANES, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
-  LAUNCH(KC_SCATTER, k_place, vgrid, VB, c);
-  LAUNCH(KC_LANESORT_SWEEP, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
+  LAUNCH(KC_PLACE, k_place, vgrid, VB, c);
+  LAUNCH(KC_LANEFIX, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
   // Fixed-time signals, the clock and the due list do not depend on vehicle
   // positions: with a fixed-time controller they run on a parallel branch
   // beside the revert resolution (joined before the injection section).

@@ -1,18 +1,21 @@
 // kernels.cu -- the per-step device pipeline of the MOSS vehicle loop.
 //
 // One step (World.step, trafficsim/engine/world.py:659-689) is the sequence
+// (engine.cu issue_step builds it into one CUDA graph)
 //
-//   k_update    A -> B     prepare-consumer + update + lane/road transitions
-//                          (world.py:261-419, 443-499), fused lane histogram
-//   k_scan      cnt -> C_start
-//   k_scatter   B -> D     bucket by post-delta lane
-//   k_lanesort  D -> C     per-lane sort by (s desc, id asc) + tentative
-//                          collision sweep (world.py:509-559)
-//   k_resolve   C          exact revert chains (rare, single thread)
-//   k_signals              world.py:619-647, time += dt, step_no++
-//   k_inject_*             world.py:561-617, per origin lane
-//   k_regroup_* C -> A'    only when membership/order changed
-//   k_speeds               world.py:649-657
+//   k_begin_step            zero lane counts, reset the step scalars
+//   k_speeds   (branch)     world.py:649-657 on the previous snapshot
+//   k_update       A -> B   prepare-consumer + update + lane/road transitions
+//                           (world.py:261-419, 443-499), lane counts
+//   k_scan                  cnt -> C lane starts (+ lane ranges)
+//   k_place        B -> C   stayers to their slot, movers to their lane's tail
+//   k_lanefix      C        per-lane sort by (s desc, id asc) + tentative
+//                           collision sweep (world.py:509-559) of flagged lanes
+//   k_signals, k_conn_flags, k_inject_due   (branch) world.py:619-647, 561-573
+//   k_resolve_fast C        exact revert chains, one warp per event
+//   k_regroup      C -> A'  C with the dirty lanes rebuilt into its tail
+//   RARE (IF node, branch): k_resolve_closure/_comp/k_resolve (meeting revert
+//       chains), k_inject_* (world.py:561-617), full regroup
 //
 // The snapshot layout A is the reference's per-lane index itself
 // (world.py:227-242): vehicles grouped by lane, s descending, id ascending,
