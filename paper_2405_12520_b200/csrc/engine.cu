@@ -333,7 +333,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_set_na, 1, 1, c, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_scatter, vgrid, VB, c, SEL_C, &dy->n_c, &dy->n_inj, SEL_A, &dy->full_regroup);
   LAUNCH(KC_REGROUP, k_lanesort<false>, wgrid, VB, c, SEL_A, &dy->full_regroup);
-  LAUNCH(KC_MISC, k_patch_finish, 1, 1024, c);
+  LAUNCH(KC_MISC, k_full_finish, 1, 1024, c);
   cond_end(e);
   if (fork_rare) {
     cudaEventRecord(e->ev_join3, e->side3);
@@ -359,7 +359,9 @@ static int sync_dyn(tsb_engine* e) {
   CK(cudaMemcpyAsync(e->dyn_host, e->c.dyn, sizeof(Dyn), cudaMemcpyDeviceToHost, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   if (e->dyn_host->overflow)
-    return fail(TSB_ECAP, "engine capacity/consistency flag 0x%x set (speed windows or host-route state)",
+    return fail(TSB_ECAP,
+                "engine capacity/consistency flag 0x%x set (0x2 speed windows, 0x4 host reroute outside split mode, "
+                "0x10 a sharded revert chain left the exact zone, 0x20 regroup path, 0x40 ghost capacity)",
                 e->dyn_host->overflow);
   return TSB_OK;
 }

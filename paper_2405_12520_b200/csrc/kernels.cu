@@ -2496,7 +2496,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) 
 }
 
 // End of a step whose snapshot the full regroup rebuilt.
-__global__ void k_patch_finish(Ctx c) {
+__global__ void k_full_finish(Ctx c) {
   PDL_WAIT();
   if (!c.dyn->full_regroup) return;  // k_regroup ended it (eager mode runs this section)
   regroup_finish(c);
