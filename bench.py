@@ -289,7 +289,8 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     ws, rank, local, pg = dist_setup()
-    workload = (f"M1: generate_grid(100,100,block_length=400,lanes_per_direction=3), "
+    tag = {(1_000_000, 29.0): "M1", (2_000_000, 22.0): "C4"}.get((args.vehicles, args.spacing), "custom")
+    workload = (f"{tag}: generate_grid(100,100,block_length=400,lanes_per_direction=3), "
                 f"{args.vehicles} pre-placed routable vehicles (slots every {args.spacing:g} m), "
                 f"EngineConfig() defaults, seed 42")
     n_gpus = ws if ws > 1 else args.gpus
