@@ -1660,14 +1660,15 @@ __device__ void rare_if_unpatchable(const Ctx& c) {
 // during the replay is a member of some closure lane's C segment (a revert
 // only moves a vehicle back to its snapshot lane, which is in the closure),
 // so the warp stages all of them once, during the closure search, and the
-// replay reads and updates the staged copy, writing every change through to
-// C (the lanes are this warp's alone: claimed).  Same algorithm, same
-// arithmetic as replay() / resolve_lane().
+// replay reads and updates the staged copy; rf_writeback copies the result
+// to C once the closures are known to be disjoint (the lanes are then this
+// warp's alone).  Same algorithm, same arithmetic as replay() /
+// resolve_lane().
 static constexpr int RF_CACHE = 192;
 struct RfE {
   double s, v, snap_s;
   int32_t j, vix, lane, snap_lane, snap_rptr, src;
-  int32_t reverted, pad;
+  int32_t reverted, rev_from;
 };
 struct RfSmem {
   union {
@@ -1682,8 +1683,8 @@ struct RfSmem {
   };
 };
 
-// resolve_lane() on the staged members; returns the cache index of the
-// vehicle to revert, or -1 (same value in every thread).
+// resolve_lane() on the staged members (results stay staged); returns the
+// cache index of the vehicle to revert, or -1 (same value in every thread).
 __device__ int32_t resolve_lane_cached(const Ctx& c, VRec* C, int32_t L, RfE* E, int32_t ncache, int16_t* i1,
                                        int16_t* i2) {
   const int lid = threadIdx.x & 31;
@@ -1732,19 +1733,15 @@ __device__ int32_t resolve_lane_cached(const Ctx& c, VRec* C, int32_t L, RfE* E,
       prev_rear = x.s - p.L;
     }
   }
-  __syncwarp();
-  for (int a = lid; a < n; a += 32) {
-    const RfE& x = E[i2[a]];
-    C[x.j].s = x.s;
-    C[x.j].v = x.v;
-  }
   rev = __shfl_sync(0xffffffffu, rev, 0);
   __syncwarp();
   return rev;
 }
 
 // replay() on the staged members, with the per-lane replay flags on chip
-// too (closure lanes q[0, qn), flags fl[]; E = the one event lane).
+// too (closure lanes q[0, qn), flags fl[]; E = the one event lane).  Nothing
+// outside shared memory is written: the replay runs before the launch's
+// warps know whether their closures met, and rf_writeback publishes it.
 enum : uint8_t { RF_INWORK = 1, RF_TOUCHED = 2 };
 __device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& R, RfE* E, int32_t ncache,
                               int16_t* i1, int16_t* i2, const int32_t* q, uint8_t* fl, int32_t ev_lane,
@@ -1787,14 +1784,8 @@ __device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& 
       x.s = x.snap_s;
       x.v = 0.0;
       x.reverted = 1;
-      VRec& r = C[x.j];
-      r.lane = Lb;
-      r.s = x.snap_s;
-      r.v = 0.0;
-      r.rptr = x.snap_rptr;
+      x.rev_from = L;  // membership change for the regroup, applied by rf_writeback
       R.moved[R.nmoved++] = x.j;
-      atomicAdd(&c.cdelta[L], -1);  // membership change for the regroup
-      atomicAdd(&c.cdelta[Lb], 1);
       uint8_t& fb = fl[qi(Lb)];
       if (!(fb & RF_TOUCHED)) {
         fb |= RF_TOUCHED;
@@ -1825,14 +1816,32 @@ __device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& 
           const VRec o = c.B[x.src];
           x.s = o.s;
           x.v = o.v;
-          C[x.j].s = o.s;
-          C[x.j].v = o.v;
         }
       }
     }
     __syncwarp();
     if (__shfl_sync(0xffffffffu, stop, 0)) break;
   }
+}
+
+// Publishes a staged replay: every staged member's state to C (reverted ones
+// with their snapshot lane and route position) and the lane membership
+// deltas of the reverts.
+__device__ void rf_writeback(const Ctx& c, VRec* C, const RfE* E, int32_t ncache) {
+  const int lid = threadIdx.x & 31;
+  for (int32_t k = lid; k < ncache; k += 32) {
+    const RfE& x = E[k];
+    VRec& r = C[x.j];
+    r.s = x.s;
+    r.v = x.v;
+    if (x.reverted) {
+      r.lane = x.lane;
+      r.rptr = x.snap_rptr;
+      atomicAdd(&c.cdelta[x.rev_from], -1);
+      atomicAdd(&c.cdelta[x.lane], 1);
+    }
+  }
+  __syncwarp();
 }
 
 // The common case without the closure kernel: every event's closure is
@@ -1913,7 +1922,7 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
       const unsigned vm = __ballot_sync(0xffffffffu, j < j1);
       const int slot = ncache + __popc(vm & ((1u << lid) - 1));
       if (j < j1 && slot < RF_CACHE)
-        cache[slot] = RfE{r.s, r.v, sn.s, j, r.vix, L, sn.lane, sn.rptr, r.src, 0, 0};
+        cache[slot] = RfE{r.s, r.v, sn.s, j, r.vix, L, sn.lane, sn.rptr, r.src, 0, -1};
       ncache += __popc(vm);
       const bool entered = T != L;
       const unsigned em = __ballot_sync(0xffffffffu, entered);
@@ -1944,6 +1953,23 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   unsigned long long t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
 #endif
+  // a staged closure is replayed at once, on chip, while the other warps
+  // are still searching: it is published only if no closures met
+  Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
+  const bool staged = ncache <= RF_CACHE;
+  if (!bad && staged) {
+    if (lid == 0) {
+      for (int k = 0; k < qn; k++) sfl[w][k] = 0;
+      sfl[w][0] = RF_INWORK;  // q[0] == E
+      heap_push(R.heap, R.hn, E);
+    }
+    __syncwarp();
+    replay_cached(c, C, CS, R, cache, ncache, U[w].k.i1, U[w].k.i2, q, sfl[w], E, (int64_t)dy->n_c + 2);
+  }
+#ifdef TSB_RF_TRACE
+  unsigned long long t2;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+#endif
   if (lid == 0) {
     if (bad) atomicExch(&dy->rf_conflict, 1);
     __threadfence();
@@ -1964,32 +1990,22 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     dy->rf_done = 1;  // read by the general path's kernels in eager mode
     dy->n_resolve_fast++;
   }
-  Replay R{0, sh[w], 0, -1, smv[w], 0, stl[w], 0, 0};
-  const bool staged = ncache <= RF_CACHE;
-  if (lid == 0) {
-    if (staged) {
-      for (int k = 0; k < qn; k++) sfl[w][k] = 0;
-      sfl[w][0] = RF_INWORK;  // q[0] == E
-    } else {
+  if (staged) {
+    rf_writeback(c, C, cache, ncache);
+  } else {
+    if (lid == 0) {
       c.rs_event[E] = 1;
       c.rs_inwork[E] = 1;
+      heap_push(R.heap, R.hn, E);
     }
-    heap_push(R.heap, R.hn, E);
-  }
-  __syncwarp();
-#ifdef TSB_RF_TRACE
-  unsigned long long t2;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-#endif
-  if (staged)
-    replay_cached(c, C, CS, R, cache, ncache, U[w].k.i1, U[w].k.i2, q, sfl[w], E, (int64_t)dy->n_c + 2);
-  else
+    __syncwarp();
     replay(c, C, CS, A, R, U[w].g.m, U[w].g.t, (int64_t)dy->n_c + 2);
+  }
 #ifdef TSB_RF_TRACE
   unsigned long long t3;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
   if (lid == 0)
-    printf("RF step %lld ev %d/%d E %d qn %d edges %d lanes_touched %d reverts %lld bfs %llu wait %llu replay %llu ns\n",
+    printf("RF step %lld ev %d/%d E %d qn %d edges %d lanes_touched %d reverts %lld bfs %llu replay %llu wait+publish %llu ns\n",
            (long long)dy->step_no, ev, ne, E, qn, nedge, R.nt, (long long)R.reverts, t1 - t0, t2 - t1, t3 - t2);
 #endif
   if (lid == 0) {
