@@ -2450,7 +2450,10 @@ __device__ void regroup_finish(const Ctx& c) {
 // block 0 publishes the lane ranges, and each warp rebuilds its lanes.  Too
 // many dirty lanes: the full regroup (the RARE body's following kernels)
 // instead, which also ends the step.  Otherwise the last block to finish ends it.
-static constexpr int RG_BLOCKS = 296;
+#ifndef RG_BLOCKS_CFG
+#define RG_BLOCKS_CFG 148
+#endif
+static constexpr int RG_BLOCKS = RG_BLOCKS_CFG;
 __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) {
   PDL_WAIT();
   Dyn* dy = c.dyn;
