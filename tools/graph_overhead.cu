@@ -25,11 +25,21 @@ __global__ void k_tiny(int* p) {
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(p, 1);
 }
 
+struct BigParam {
+  int* p;
+  char pad[1384];  // the engine's Ctx is ~1.4 KB
+};
+__global__ void k_tiny_big(BigParam b) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(b.p, 1);
+}
+
 __global__ void k_set(cudaGraphConditionalHandle h, int v) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (v) cudaGraphSetConditional(h, 1u);
 }
 
+static bool g_big = false;
 static cudaError_t launch(cudaStream_t s, bool pdl, int grid, int* p) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -40,6 +50,11 @@ static cudaError_t launch(cudaStream_t s, bool pdl, int grid, int* p) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
+  if (g_big) {
+    BigParam b{};
+    b.p = p;
+    return cudaLaunchKernelEx(&cfg, k_tiny_big, b);
+  }
   return cudaLaunchKernelEx(&cfg, k_tiny, p);
 }
 
@@ -113,6 +128,12 @@ int main() {
                     cond ? "_if" : "", us);
         first = false;
       }
+  g_big = true;
+  for (int grid : {1, 1184}) {
+    float us;
+    if (run(32, true, false, grid, &us)) return 1;
+    std::printf(", \"grid%d_pdl_1400B_params\": %.2f", grid, us);
+  }
   std::printf("}}\n");
   return 0;
 }
