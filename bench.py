@@ -107,6 +107,7 @@ def run_sharded(args, ws, rank, local, pg, workload):
     own = int((sw.plan.zone & 1).sum())
     halo = int(((sw.plan.zone & 2) > 0).sum())
     xbytes = sw.exchanged_bytes
+    used_p2p, p2p_err = sw.p2p, sw.p2p_error
     sw.close()
     if rank != 0:
         return
@@ -119,8 +120,9 @@ def run_sharded(args, ws, rank, local, pg, workload):
                    "parallelism": f"lane bands x{ws} (sharded.py; halo lanes rank0: {halo} vs own {own})",
                    "exchange": ("per step: pack kernel writes boundary-lane packets into the peers' "
                                 "IPC-mapped receive slots (NVLink P2P), release/acquire flags, ghost import; "
-                                "no host synchronisation" if p2p else
-                                "per step: NCCL all_to_all_single of boundary-lane packets + counters"),
+                                "no host synchronisation" if used_p2p else
+                                "per step: NCCL all_to_all_single of boundary-lane packets + counters"
+                                + (f" (P2P mapping failed: {p2p_err})" if p2p and not used_p2p else "")),
                    "exchanged_bytes_rank0_total": xbytes,
                    "timing": "engine-stream events around K steps incl. exchanges, max over ranks"},
         "e2e": {"value": (u2 - u1) / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": 0,

@@ -105,8 +105,22 @@ class ShardedWorld:
                                  device=self.device)
         self.exchanged_bytes = 0
         self.p2p = p2p
+        self.p2p_error = None
         if p2p:
-            self._setup_p2p()
+            # every rank maps every peer's memory, or all fall back to the
+            # collective transport together (e.g. no peer access between
+            # the devices)
+            ok = 1
+            try:
+                self._setup_p2p()
+            except Exception as exc:  # noqa: BLE001 -- reported, then the fallback
+                ok = 0
+                self.p2p_error = repr(exc)
+            t = torch.tensor([ok], dtype=torch.int64)
+            if not host_staging:
+                t = t.to(self.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            self.p2p = bool(int(t.item()))  # (the all-reduce also orders every mapping before the first exchange)
         self._exchange()  # initial ghosts (empty network: zero vehicles)
 
     def _setup_p2p(self):
@@ -130,7 +144,6 @@ class ShardedWorld:
             _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(bf), C.byref(b)))
             pr[q], pf[q] = a, b
         _native.check(L.tsb_shard_p2p_set_peers(self._h, pr, pf))
-        self.dist.barrier(group=self.group)  # every rank mapped before the first exchange
 
     @classmethod
     def from_network(cls, net, trips, config=None, seed=0, rank=0, nranks=1, device=0, group=None,
