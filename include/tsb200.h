@@ -142,10 +142,12 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes);
  * *slot_bytes) and arrival flags (2 x nranks u64), both cudaMalloc bases, so
  * tsb_ipc_handle can export them; every rank opens its peers' with
  * tsb_ipc_open and passes them (rank order, own entry ignored) to
- * tsb_shard_p2p_set_peers.  tsb_shard_p2p_exchange then enqueues, on the
- * engine stream and without a host synchronisation, the pack written
- * straight into each peer's slot, a release of the peer's flag, the wait
- * for every peer's flag and the ghost import. */
+ * tsb_shard_p2p_set_peers.  From then on every step (tsb_step, in the step
+ * graph) ends with the exchange: the pack written straight into each peer's
+ * slot, a release of the peer's flag, the wait for every peer's flag and the
+ * ghost import -- on the engine stream, no host synchronisation.
+ * tsb_shard_p2p_exchange enqueues one exchange on its own (the initial
+ * ghosts, before the first step). */
 int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes);
 int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags);
 int tsb_shard_p2p_exchange(tsb_engine* e);

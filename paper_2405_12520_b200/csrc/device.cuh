@@ -127,6 +127,7 @@ struct Dyn {
   int32_t tl_row;       // TSB_TIMELINE builds: the step's row in the timeline ring
   int32_t rare;         // the step takes the RARE body (set_rare)
   int32_t pad4_;
+  unsigned long long xchg_epoch;  // sharded P2P exchanges so far (k_exp_count)
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };

@@ -102,7 +102,7 @@ struct tsb_engine {
   cudaStream_t cond_on = nullptr;  // stream a conditional node is being captured on
   cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
   uint8_t* p2p_recv = nullptr;        // own receive slots (device-driven exchange)
-  unsigned long long p2p_epoch = 0;   // exchanges so far
+  bool p2p_ready = false;             // peers mapped: every step ends with the exchange
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
@@ -235,6 +235,28 @@ static void cond_end(tsb_engine* e) {
   e->cur = e->cond_on;
 }
 
+// Sharded engine with mapped peers: the ghost exchange over peer memory
+// (kernels.cu k_exp_pack_p2p), the epoch kept on the device so the sequence
+// can be part of the step graph.
+static void issue_exchange(tsb_engine* e, Launcher& L) {
+  Ctx& c = e->c;
+  const int VB = 256;
+  LAUNCH(KC_MISC, k_exp_count, grid_for(std::max(c.n_exp, 1), VB, 1 << 20), VB, c, 1);
+  if (c.n_exp > 0) {
+    scan(e, L, KC_MISC, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE, nullptr, c.n_exp, c.n_exp, nullptr);
+    LAUNCH(KC_MISC, k_exp_pack_p2p, grid_for((int64_t)c.n_exp * 32, VB, 1 << 20), VB, c);
+  }
+  LAUNCH(KC_MISC, k_p2p_signal, 1, 32, c);
+  LAUNCH(KC_MISC, k_p2p_wait, 1, 32, c);
+  if (c.n_imp > 0) {
+    SrcBase sb{};
+    sb.b[0] = -1;  // slots of the current epoch (kernels.cu src_base)
+    LAUNCH(KC_MISC, k_imp_count, grid_for(c.n_imp, VB, 1 << 20), VB, c, (const uint8_t*)e->p2p_recv, sb);
+    scan(e, L, KC_MISC, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE, nullptr, c.n_imp, c.n_imp, nullptr);
+    LAUNCH(KC_MISC, k_imp_copy, grid_for((int64_t)c.n_imp * 32, VB, 1 << 20), VB, c, (const uint8_t*)e->p2p_recv, sb);
+  }
+}
+
 // phase 0 = whole step; 1 = through k_update; 2 = the rest (split mode).
 static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   Ctx& c = e->c;
@@ -342,6 +364,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 0);
   if (fork_rare) cudaStreamWaitEvent(e->cur, e->ev_join3, 0);
   if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
+  if (c.sharded && e->p2p_ready) issue_exchange(e, L);
 }
 
 // Accumulates the current snapshot's road aggregate if the next step has not
@@ -1062,7 +1085,7 @@ int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes) {
   if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
   Ctx& c = e->c;
   if (c.n_exp > 0) {
-    k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, e->stream>>>(c);
+    k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, e->stream>>>(c, 0);
     const int ntiles = c.n_exp / SCAN_TILE + 1;
     k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, e->stream>>>(c, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE,
                                                                  nullptr, c.n_exp, ntiles, nullptr);
@@ -1153,33 +1176,15 @@ int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* 
     c.p2p_peer_recv[q] = (uint8_t*)peer_recv[q];
     c.p2p_peer_flag[q] = (unsigned long long*)peer_flags[q];
   }
-  e->graph_dirty = true;  // Ctx is captured by value
+  e->p2p_ready = true;
+  e->graph_dirty = true;  // Ctx is captured by value; the step graph now ends with the exchange
   return TSB_OK;
 }
 
 int tsb_shard_p2p_exchange(tsb_engine* e) {
-  if (!e || !e->c.sharded || !e->c.p2p_flag) return fail(TSB_EINVAL, "P2P exchange not set up");
-  Ctx& c = e->c;
-  const unsigned long long epoch = ++e->p2p_epoch;
-  cudaStream_t st = e->stream;
-  if (c.n_exp > 0) {
-    k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, st>>>(c);
-    const int ntiles = c.n_exp / SCAN_TILE + 1;
-    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, st>>>(c, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE, nullptr,
-                                                            c.n_exp, ntiles, nullptr);
-    k_exp_pack_p2p<<<grid_for((int64_t)c.n_exp * 32, 256, 1 << 20), 256, 0, st>>>(c, epoch);
-  }
-  k_p2p_signal<<<1, 32, 0, st>>>(c, epoch);
-  k_p2p_wait<<<1, 32, 0, st>>>(c, epoch);
-  if (c.n_imp > 0) {
-    SrcBase sb{};
-    for (int q = 0; q < c.nranks; q++) sb.b[q] = (int64_t)((epoch & 1) * c.nranks + q) * c.p2p_slot;
-    k_imp_count<<<grid_for(c.n_imp, 256, 1 << 20), 256, 0, st>>>(c, e->p2p_recv, sb);
-    const int ntiles = c.n_imp / SCAN_TILE + 1;
-    k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, st>>>(c, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE, nullptr,
-                                                            c.n_imp, ntiles, nullptr);
-    k_imp_copy<<<grid_for((int64_t)c.n_imp * 32, 256, 1 << 20), 256, 0, st>>>(c, e->p2p_recv, sb);
-  }
+  if (!e || !e->c.sharded || !e->p2p_ready) return fail(TSB_EINVAL, "P2P exchange not set up");
+  Launcher L{e};
+  issue_exchange(e, L);
   CK(cudaGetLastError());
   return TSB_OK;  // no host synchronisation: the next step follows in stream order
 }

@@ -2663,8 +2663,9 @@ __global__ void k_count_own(Ctx c) {
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&dy->n_own, mine);
 }
 
-__global__ void k_exp_count(Ctx c) {
+__global__ void k_exp_count(Ctx c, int p2p) {
   PDL_WAIT();
+  if (p2p && gtid() == 0) c.dyn->xchg_epoch += 1;  // this exchange's epoch (device-side: graph-capturable)
   const int2* S = c.rng[c.dyn->cur];
   for (int32_t e = gtid(); e < c.n_exp; e += gstride()) {
     const int32_t L = c.exp_lane[e];
@@ -2710,8 +2711,9 @@ __global__ void k_exp_pack(Ctx c, uint8_t* send) {
 // slots.  Two slot sets by step parity: a rank writes parity t+1 only after
 // its own import of step t saw every peer's step-t flag, which each peer
 // raised after importing step t-1 from that slot set.
-__global__ void k_exp_pack_p2p(Ctx c, unsigned long long epoch) {
+__global__ void k_exp_pack_p2p(Ctx c) {
   PDL_WAIT();
+  const unsigned long long epoch = c.dyn->xchg_epoch;
   const VRec* A = c.lay[c.dyn->cur];
   const int2* S = c.rng[c.dyn->cur];
   const int lid = threadIdx.x & 31;
@@ -2729,8 +2731,9 @@ __global__ void k_exp_pack_p2p(Ctx c, unsigned long long epoch) {
   }
 }
 
-__global__ void k_p2p_signal(Ctx c, unsigned long long epoch) {
+__global__ void k_p2p_signal(Ctx c) {
   PDL_WAIT();
+  const unsigned long long epoch = c.dyn->xchg_epoch;
   __threadfence_system();  // the pack's remote writes before the flags
   const int q = threadIdx.x;
   if (q < c.nranks && q != c.rank) {
@@ -2739,8 +2742,9 @@ __global__ void k_p2p_signal(Ctx c, unsigned long long epoch) {
   }
 }
 
-__global__ void k_p2p_wait(Ctx c, unsigned long long epoch) {
+__global__ void k_p2p_wait(Ctx c) {
   PDL_WAIT();
+  const unsigned long long epoch = c.dyn->xchg_epoch;
   const int q = threadIdx.x;
   if (q < c.nranks && q != c.rank) {
     const unsigned long long* f = c.p2p_flag + (epoch & 1) * c.nranks + q;
@@ -2760,11 +2764,18 @@ __global__ void k_p2p_wait(Ctx c, unsigned long long epoch) {
 struct SrcBase {
   int64_t b[9];
 };
+// Byte offset of source q's message: sb, or (P2P: sb.b[0] < 0) the slot of
+// q for the current exchange epoch's parity.
+__device__ __forceinline__ int64_t src_base(const Ctx& c, const SrcBase& sb, int q) {
+  if (sb.b[0] >= 0) return sb.b[q];
+  return (int64_t)((c.dyn->xchg_epoch & 1) * c.nranks + q) * c.p2p_slot;
+}
+
 __global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
   PDL_WAIT();
   for (int32_t e = gtid(); e < c.n_imp; e += gstride()) {
     const int q = c.imp_peer[e];
-    c.imp_cnt[e] = ((const int32_t*)(recv + sb.b[q]))[e - c.peer_first_imp[q]];
+    c.imp_cnt[e] = ((const int32_t*)(recv + src_base(c, sb, q)))[e - c.peer_first_imp[q]];
   }
 }
 
@@ -2781,7 +2792,7 @@ __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
     const int64_t e0 = c.peer_first_imp[q];
     const int32_t L = c.imp_lane[e];
     const int32_t n = c.imp_cnt[e];
-    const VRec* src = (const VRec*)(recv + sb.b[q] + align32(4 * (c.peer_first_imp[q + 1] - e0))) +
+    const VRec* src = (const VRec*)(recv + src_base(c, sb, q) + align32(4 * (c.peer_first_imp[q + 1] - e0))) +
                       (c.imp_pos[e] - c.imp_pos[e0]);
     const int32_t at = base + c.imp_pos[e];
     if ((int64_t)at + n > c.cap_rec) {  // ghost capacity (fails loudly at the next sync)

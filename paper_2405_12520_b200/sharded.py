@@ -180,14 +180,15 @@ class ShardedWorld:
 
     def step_local(self, n: int = 1):
         """n steps, exchanging ghosts after each (no global reductions)."""
-        for _ in range(n):
-            if self.p2p:  # all on the engine stream: no host synchronisation per step
-                _native.check(_native.lib().tsb_step_async(self._h, 1))
-            else:
-                _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
-            self._exchange()
         if self.p2p:
+            # the step graph ends with the exchange: n graph replays, no host
+            # synchronisation until the report
+            _native.check(_native.lib().tsb_step_async(self._h, n))
             _native.check(_native.lib().tsb_report_get(self._h, C.byref(self._report)))
+            return
+        for _ in range(n):
+            _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
+            self._exchange()
 
     def report(self) -> dict:
         """StepReport counters summed over ranks (time and step are shared)."""
