@@ -106,7 +106,7 @@ __device__ __forceinline__ void set_rare(const Ctx& c) {
 }
 
 // A lane whose membership or order changed after the sweep; the next
-// snapshot rebuilds only these lanes (k_patch_*), unless too many changed.
+// snapshot rebuilds only these lanes (k_regroup), unless too many changed.
 __device__ __forceinline__ void mark_dirty(const Ctx& c, int32_t L) {
   if (atomicExch(&c.dirty_flag[L], 1) == 0) {
     int32_t k = atomicAdd(&c.dyn->n_dirty, 1);
@@ -1118,7 +1118,7 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
 
 // ------------------------------------------------------------------ revert resolution
 //
-// k_lanesort's tentative sweep handles every lane whose sweep needs no
+// k_lanefix's tentative sweep handles every lane whose sweep needs no
 // revert.  Lanes that would revert ("events") are resolved here by
 // replaying the reference's restart-after-revert loop (world.py:518-559)
 // exactly.  The replay only ever touches lanes reachable from an event lane
@@ -1379,7 +1379,7 @@ __device__ void replay(const Ctx& c, VRec* C, const int32_t* CS, const VRec* A, 
         c.rs_touched[Lb] = 1;
         R.touched[R.nt++] = Lb;
         // the reference sweeps Lb for the first time only now, with the
-        // reverted vehicle present: undo k_lanesort's tentative sweep
+        // reverted vehicle present: undo k_lanefix's tentative sweep
         restore = (Lb > R.reach && !c.rs_event[Lb]) ? 1 : 0;
       }
       if (!c.rs_inwork[L]) {
@@ -1791,7 +1791,7 @@ __device__ void replay_cached(const Ctx& c, VRec* C, const int32_t* CS, Replay& 
         fb |= RF_TOUCHED;
         R.touched[R.nt++] = Lb;
         // the reference sweeps Lb for the first time only now, with the
-        // reverted vehicle present: undo k_lanesort's tentative sweep
+        // reverted vehicle present: undo k_lanefix's tentative sweep
         restore = (Lb > R.reach && Lb != ev_lane) ? 1 : 0;
       }
       uint8_t& fa = fl[qi(L)];
