@@ -1901,11 +1901,10 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   int32_t qn = 1, nedge = 0, ncache = 0;  // ncache > RF_CACHE: not staged (global replay)
   RfE* cache = U[w].k.e;
   bool bad = false;
-  if (lid == 0) {
-    q[0] = E;
-    bad = claim(E) < 0;
-  }
-  bad = __shfl_sync(0xffffffffu, (int)bad, 0);
+  if (lid == 0) q[0] = E;
+  __syncwarp();
+  // breadth-first over the closure with a local visited list; the lanes are
+  // claimed afterwards, all at once (one atomic round trip, not one per lane)
   for (int32_t h = 0; h < qn && !bad; h++) {
     const int32_t L = q[h];
     const int32_t j0 = CS[L], j1 = CS[L + 1];
@@ -1927,16 +1926,21 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
       const bool entered = T != L;
       const unsigned em = __ballot_sync(0xffffffffu, entered);
       nedge += __popc(em);
-      // claim the origin lanes of the entered members, all at once (two
-      // members from one lane: one claims it, the other finds it ours)
-      const int cr = entered ? claim(T) : 0;
-      if (__any_sync(0xffffffffu, cr < 0)) bad = true;
-      const unsigned nm = __ballot_sync(0xffffffffu, cr == 1);
+      // new origin lanes: one representative per distinct lane, not yet listed
+      bool fresh = false;
+      if (entered) {
+        const unsigned grp = __match_any_sync(em, T);
+        fresh = lid == __ffs(grp) - 1;
+        for (int32_t k = 0; k < qn && fresh; k++)
+          if (q[k] == T) fresh = false;
+      }
+      const unsigned nm = __ballot_sync(0xffffffffu, fresh);
       if (qn + __popc(nm) > HCAP) {
         bad = true;
-      } else if (cr == 1) {
+      } else if (fresh) {
         q[qn + __popc(nm & ((1u << lid) - 1))] = T;
       }
+      __syncwarp();
       qn += __popc(nm);
       if (qn > HCAP) qn = HCAP;
     }
@@ -1949,6 +1953,12 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   if (!bad)
     for (int32_t h = 0; h < qn; h++)
       if (CS[q[h] + 1] - CS[q[h]] + nedge > RS_CAP) bad = true;
+  // claim the closure: a lane another closure claimed first means they meet
+  if (!bad) {
+    bool lost = false;
+    for (int32_t k = lid; k < qn; k += 32) lost |= claim(q[k]) < 0;
+    if (__any_sync(0xffffffffu, lost)) bad = true;
+  }
 #ifdef TSB_RF_TRACE
   unsigned long long t1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
