@@ -239,7 +239,8 @@ int tsb_path_counters(tsb_engine* e, int64_t* out);
  * rows, slot = phase (kernels.cu TL_*), taken when the phase's kernel
  * passed its dependency wait. */
 int tsb_timeline(tsb_engine* e, uint64_t* out);
-/* Kernel launches issued per step (for the bench's gpu_launches claim). */
+/* Kernel launches every step issues (for the bench's gpu_launches claim):
+ * the step graph's kernels outside its conditional (RARE) body. */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);
 
 #ifdef __cplusplus

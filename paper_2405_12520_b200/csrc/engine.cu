@@ -149,12 +149,14 @@ struct Launcher {
       cudaEventRecord(e->ev[2 * e->n_ev], e->stream);
     }
   }
+  int in_body = 0;  // launches inside a conditional body (they run only when its condition holds)
   void post() {
     if (e->profiling && e->n_ev < 96) {
       cudaEventRecord(e->ev[2 * e->n_ev + 1], e->stream);
       e->n_ev++;
     }
     count++;
+    if (e->capturing && e->cur == e->body) in_body++;
   }
 };
 
@@ -658,7 +660,7 @@ static int capture_steps(tsb_engine* e, int copies, cudaGraph_t* graph, cudaGrap
   CK(er);
   *graph = g;
   CK(cudaGraphInstantiate(exec, *graph, 0));
-  *launches = L.count / copies;
+  *launches = (L.count - L.in_body) / copies;  // the kernels every step launches
   return TSB_OK;
 }
 
