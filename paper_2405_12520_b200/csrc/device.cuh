@@ -194,6 +194,7 @@ struct Ctx {
   int32_t* fix_list;
   unsigned long long* scan_status;   // SCAN_SITES regions of scan_tiles_cap words
   unsigned long long* scan_tickets;  // per scan site, never reset
+  int32_t* scan_tile_sums;           // per tile totals of the two-pass lane scan
   int32_t scan_tiles_cap;
   // sharded mode (shard.py): per-lane zone flags, ghost ranges, export/import lists
   int32_t sharded;

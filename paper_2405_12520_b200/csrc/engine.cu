@@ -200,7 +200,8 @@ static void scan(tsb_engine* e, Launcher& L, int kc, int site, const int32_t* in
                  const int32_t* n_dev, int32_t n_static, int64_t n_max, const int32_t* gate) {
   Ctx& c = e->c;
   const int ntiles = (int)(n_max / SCAN_TILE + 1);
-  LAUNCH(kc, (k_scan<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, site, in, out, out_sel, n_dev, n_static, ntiles, gate);
+  LAUNCH(kc, (k_scan<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, site, in, out, out_sel, n_dev, n_static, ntiles, gate,
+         (const int32_t*)nullptr);
 }
 
 // Conditional section (graph capture only): an IF node on handle c.cond[k]
@@ -290,7 +291,14 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
   // bucket the post-delta state by lane, sort each lane, tentative sweep
-  scan(e, L, KC_SCAN, SCAN_LANES, c.cnt, nullptr, SEL_C, nullptr, NL, NL, nullptr);
+  {
+    // two passes (tile totals, then tiles with their prefixes): no serial look-back
+    const int ntiles = (int)(NL / SCAN_TILE + 1);
+    LAUNCH(KC_SCAN, (k_tile_sums<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, (const int32_t*)c.cnt, NL, c.scan_tile_sums);
+    LAUNCH(KC_SCAN, (k_scan<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, SCAN_LANES, (const int32_t*)c.cnt,
+           (int32_t*)nullptr, SEL_C, (const int32_t*)nullptr, NL, ntiles, (const int32_t*)nullptr,
+           (const int32_t*)c.scan_tile_sums);
+  }
   LAUNCH(KC_PLACE, k_place, vgrid, VB, c);
   LAUNCH(KC_LANEFIX, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
   // Fixed-time signals, the clock and the due list do not depend on vehicle
@@ -1006,6 +1014,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.fix_flag, NL));
   RC(dalloc(E, &c.fix_list, NL));
   c.scan_tiles_cap = (int32_t)(std::max<int64_t>(NL, CAP) / SCAN_TILE + 2);
+  RC(dalloc(E, &c.scan_tile_sums, (size_t)c.scan_tiles_cap));
   RC(dalloc(E, &c.scan_status, (size_t)SCAN_SITES * c.scan_tiles_cap));
   RC(dalloc(E, &c.scan_tickets, SCAN_SITES));
   RC(dalloc(E, &c.stage, (size_t)NL + 1));
@@ -1090,7 +1099,7 @@ int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes) {
     k_exp_count<<<grid_for(c.n_exp, 256, 1 << 20), 256, 0, e->stream>>>(c, 0);
     const int ntiles = c.n_exp / SCAN_TILE + 1;
     k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, e->stream>>>(c, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE,
-                                                                 nullptr, c.n_exp, ntiles, nullptr);
+                                                                 nullptr, c.n_exp, ntiles, nullptr, nullptr);
   }
   std::vector<int32_t> pos(c.n_exp + 1, 0);
   if (c.n_exp > 0) CK(cudaMemcpyAsync(pos.data(), c.exp_pos, sizeof(int32_t) * (c.n_exp + 1), cudaMemcpyDeviceToHost, e->stream));
@@ -1123,7 +1132,7 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes) {
     k_imp_count<<<grid_for(c.n_imp, 256, 1 << 20), 256, 0, e->stream>>>(c, (const uint8_t*)recv, sb);
     const int ntiles = c.n_imp / SCAN_TILE + 1;
     k_scan<SCAN_BT, SCAN_IPT><<<ntiles, SCAN_BT, 0, e->stream>>>(c, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE,
-                                                                 nullptr, c.n_imp, ntiles, nullptr);
+                                                                 nullptr, c.n_imp, ntiles, nullptr, nullptr);
     k_imp_copy<<<grid_for((int64_t)c.n_imp * 32, 256, 1 << 20), 256, 0, e->stream>>>(c, (const uint8_t*)recv, sb);
   }
   CK(cudaGetLastError());

@@ -632,12 +632,38 @@ __global__ void k_count_hostq(Ctx c) {
 // blocks must be launched and draw a ticket (the gate is grid-uniform).
 static constexpr int SCAN_SITES = 6;
 enum { SCAN_LANES = 0, SCAN_INJ_LANES = 1, SCAN_INJ_RETRY = 2, SCAN_REGROUP = 3, SCAN_EXPORT = 4, SCAN_IMPORT = 5 };
+// Two-pass form for the step's lane scan: k_tile_sums writes each tile's
+// total, then k_scan (tile_sums != nullptr) takes tile b's prefix as the sum
+// of the totals before it -- no serial look-back chain across 150+ tiles.
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) k_tile_sums(Ctx c, const int32_t* in, int32_t n, int32_t* sums) {
+  PDL_WAIT();
+  if (blockIdx.x == 0) TL_MARK(TL_SCAN);
+  const int64_t base = (int64_t)blockIdx.x * BT * IPT;
+  int32_t local = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; k++) {
+    const int64_t idx = base + (int64_t)k * BT + threadIdx.x;  // coalesced
+    local += idx < n ? in[idx] : 0;
+  }
+  __shared__ int32_t s_w[BT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int w = 0; w < BT / 32; w++) t += s_w[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in, int32_t* out, int out_sel,
                                              const int32_t* n_dev, int32_t n_static, int32_t ntiles,
-                                             const int32_t* gate) {
+                                             const int32_t* gate, const int32_t* tile_sums) {
   PDL_WAIT();
-  if (site == SCAN_LANES) TL_MARK(TL_SCAN);
+  if (site == SCAN_LANES && !tile_sums) TL_MARK(TL_SCAN);
   if (gated_off(gate)) return;
   int2* rng = nullptr;
   if (out_sel != SEL_NONE) {
@@ -650,9 +676,14 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
   __shared__ unsigned s_epoch;
   __shared__ int32_t s_warp[BT / 32];
   if (threadIdx.x == 0) {
-    const unsigned long long t = atomicAdd(c.scan_tickets + site, 1ULL);
-    s_tile = (int32_t)(t % (unsigned long long)ntiles);
-    s_epoch = (unsigned)((t / (unsigned long long)ntiles) % 0x3fffffffULL) + 1u;
+    if (tile_sums) {
+      s_tile = blockIdx.x;
+      s_epoch = 1u;
+    } else {
+      const unsigned long long t = atomicAdd(c.scan_tickets + site, 1ULL);
+      s_tile = (int32_t)(t % (unsigned long long)ntiles);
+      s_epoch = (unsigned)((t / (unsigned long long)ntiles) % 0x3fffffffULL) + 1u;
+    }
   }
   __syncthreads();
   const int32_t tile = s_tile;
@@ -693,7 +724,15 @@ __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in,
   // status word: epoch (30 bits) | flag (2 bits) | value (32 bits);
   // flag 1 = tile aggregate, 2 = inclusive prefix
   volatile unsigned long long* st = status;
-  if (tile == 0) {
+  if (tile_sums) {
+    if (warp == 0) {
+      int32_t acc = 0;
+      for (int32_t t = lane; t < tile; t += 32) acc += tile_sums[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) s_prefix = acc;
+    }
+  } else if (tile == 0) {
     if (threadIdx.x == 0) {
       __threadfence();
       st[0] = ep | (2ULL << 32) | (unsigned)total;
