@@ -1744,11 +1744,18 @@ __device__ int32_t resolve_lane_cached(const Ctx& c, VRec* C, int32_t L, RfE* E,
     i2[rank] = i1[a];
   }
   __syncwarp();
+  // the sweep changes nothing before its first trigger: find it in
+  // parallel, then run the sequential sweep from there (same arithmetic)
+  int first = n;
+  for (int a = lid; a < n; a += 32)
+    if (a > 0 && E[i2[a]].s > ((E[i2[a - 1]].s - p.L) - p.s0_floor) + 1e-12) first = min(first, a);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
   int32_t rev = -1;
-  if (lid == 0) {
-    int prev = -1;
-    double prev_rear = CUDART_INF;
-    for (int a = 0; a < n; a++) {
+  if (lid == 0 && first < n) {
+    int prev = first - 1;
+    double prev_rear = E[i2[prev]].s - p.L;
+    for (int a = first; a < n; a++) {
       RfE& x = E[i2[a]];
       const double limit = prev_rear - p.s0_floor;
       const bool entered = x.snap_lane != L;
