@@ -151,10 +151,12 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes);
 int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes);
 int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags);
 int tsb_shard_p2p_exchange(tsb_engine* e);
-/* cudaIpcGetMemHandle / cudaIpcOpenMemHandle (64-byte handles). */
+/* cudaIpcGetMemHandle / cudaIpcOpenMemHandle / cudaIpcCloseMemHandle
+ * (64-byte handles). */
 #define TSB_IPC_HANDLE_BYTES 64
 int tsb_ipc_handle(const void* dev_ptr, uint8_t* handle);
 int tsb_ipc_open(const uint8_t* handle, void** dev_ptr);
+int tsb_ipc_close(void* dev_ptr);
 
 /* World.step() x n (world.py:659-689); report of the last step (may be NULL). */
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last);

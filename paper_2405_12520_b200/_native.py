@@ -60,6 +60,7 @@ SIGNATURES = {
     "tsb_step_async": (_i32, [_vp, _i32]),
     "tsb_ipc_handle": (_i32, [_vp, _vp]),
     "tsb_ipc_open": (_i32, [_vp, _vp]),
+    "tsb_ipc_close": (_i32, [_vp]),
 }
 
 _lib = None

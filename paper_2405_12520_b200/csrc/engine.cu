@@ -1179,6 +1179,11 @@ int tsb_ipc_open(const uint8_t* handle, void** dev_ptr) {
   return TSB_OK;
 }
 
+int tsb_ipc_close(void* dev_ptr) {
+  CK(cudaIpcCloseMemHandle(dev_ptr));
+  return TSB_OK;
+}
+
 int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags) {
   if (!e || !e->c.sharded || !e->c.p2p_flag) return fail(TSB_EINVAL, "call tsb_shard_p2p_alloc first");
   Ctx& c = e->c;

@@ -106,6 +106,7 @@ class ShardedWorld:
         self.exchanged_bytes = 0
         self.p2p = p2p
         self.p2p_error = None
+        self._ipc_mapped = []  # peer buffers opened through CUDA IPC (closed in close())
         if p2p:
             # every rank maps every peer's memory, or all fall back to the
             # collective transport together (e.g. no peer access between
@@ -141,7 +142,9 @@ class ShardedWorld:
                 continue
             a, b = C.c_void_p(), C.c_void_p()
             _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(br), C.byref(a)))
+            self._ipc_mapped.append(a)
             _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(bf), C.byref(b)))
+            self._ipc_mapped.append(b)
             pr[q], pf[q] = a, b
         _native.check(L.tsb_shard_p2p_set_peers(self._h, pr, pf))
 
@@ -156,8 +159,12 @@ class ShardedWorld:
 
     def close(self):
         if self._h is not None:
-            _native.lib().tsb_destroy(self._h)
+            L = _native.lib()
+            L.tsb_destroy(self._h)  # (synchronises the device: no kernel still uses the mappings)
             self._h = None
+            for ptr in getattr(self, "_ipc_mapped", []):
+                L.tsb_ipc_close(ptr)
+            self._ipc_mapped = []
 
     __del__ = close
 
