@@ -295,7 +295,7 @@ def main():
     workload = (f"{tag}: generate_grid(100,100,block_length=400,lanes_per_direction=3), "
                 f"{args.vehicles} pre-placed routable vehicles (slots every {args.spacing:g} m), "
                 f"EngineConfig() defaults, seed 42")
-    n_gpus = ws if ws > 1 else args.gpus
+    n_gpus = ws  # processes actually running (one per GPU); --gpus N without torchrun runs one
 
     if args.impl == "reference":
         if rank != 0:
