@@ -1029,7 +1029,10 @@ __global__ void k_place(Ctx c) {
   }
 }
 
-static constexpr int LX_CAP = 64;   // lane members staged in shared memory
+#ifndef LX_CAP_CFG
+#define LX_CAP_CFG 64
+#endif
+static constexpr int LX_CAP = LX_CAP_CFG;  // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   PDL_WAIT();
