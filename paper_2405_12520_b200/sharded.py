@@ -108,45 +108,61 @@ class ShardedWorld:
         self.p2p_error = None
         self._ipc_mapped = []  # peer buffers opened through CUDA IPC (closed in close())
         if p2p:
-            # every rank maps every peer's memory, or all fall back to the
-            # collective transport together (e.g. no peer access between
-            # the devices)
-            ok = 1
-            try:
-                self._setup_p2p()
-            except Exception as exc:  # noqa: BLE001 -- reported, then the fallback
-                ok = 0
-                self.p2p_error = repr(exc)
-            t = torch.tensor([ok], dtype=torch.int64)
-            if not host_staging:
-                t = t.to(self.device)
-            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
-            self.p2p = bool(int(t.item()))  # (the all-reduce also orders every mapping before the first exchange)
+            # every rank maps every peer's memory, or all keep the collective
+            # transport together (e.g. no peer access between the devices)
+            self.p2p = self._setup_p2p()
         self._exchange()  # initial ghosts (empty network: zero vehicles)
 
-    def _setup_p2p(self):
+    def _agree(self, ok: bool) -> bool:
+        """True iff every rank says ok (one all-reduce, every rank calls)."""
+        t = self.torch.tensor([1 if ok else 0], dtype=self.torch.int64)
+        if not self.host_staging:
+            t = t.to(self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
+
+    def _setup_p2p(self) -> bool:
         """Receive slots and arrival flags of every rank mapped into every
-        other rank (CUDA IPC handles exchanged once through the process group)."""
+        other rank (CUDA IPC handles exchanged once through the process
+        group).  Every rank runs the same collectives whatever fails locally;
+        the engines switch to the device exchange only if every rank mapped
+        every peer (else all keep the collective transport)."""
+        import os
+
         L = _native.lib()
         recv, flags, slot = C.c_void_p(), C.c_void_p(), C.c_int64()
-        _native.check(L.tsb_shard_p2p_alloc(self._h, C.byref(recv), C.byref(flags), C.byref(slot)))
         hr, hf = (C.c_uint8 * 64)(), (C.c_uint8 * 64)()
-        _native.check(L.tsb_ipc_handle(recv, hr))
-        _native.check(L.tsb_ipc_handle(flags, hf))
+        ok = True
+        try:
+            if os.environ.get("TSB_P2P_FAIL_RANK") == str(self.rank):  # test hook: this rank cannot map
+                raise RuntimeError("P2P mapping disabled by TSB_P2P_FAIL_RANK")
+            _native.check(L.tsb_shard_p2p_alloc(self._h, C.byref(recv), C.byref(flags), C.byref(slot)))
+            _native.check(L.tsb_ipc_handle(recv, hr))
+            _native.check(L.tsb_ipc_handle(flags, hf))
+        except Exception as exc:  # noqa: BLE001 -- reported, then the fallback
+            ok, self.p2p_error = False, repr(exc)
         got = [None] * self.nranks
-        self.dist.all_gather_object(got, (bytes(hr), bytes(hf)), group=self.group)
+        self.dist.all_gather_object(got, (ok, bytes(hr), bytes(hf)), group=self.group)
+        if not all(g[0] for g in got):
+            return False
         pr, pf = (C.c_void_p * self.nranks)(), (C.c_void_p * self.nranks)()
-        for q, (br, bf) in enumerate(got):
-            if q == self.rank:
-                pr[q], pf[q] = recv, flags
-                continue
-            a, b = C.c_void_p(), C.c_void_p()
-            _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(br), C.byref(a)))
-            self._ipc_mapped.append(a)
-            _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(bf), C.byref(b)))
-            self._ipc_mapped.append(b)
-            pr[q], pf[q] = a, b
+        try:
+            for q, (_, br, bf) in enumerate(got):
+                if q == self.rank:
+                    pr[q], pf[q] = recv, flags
+                    continue
+                a, b = C.c_void_p(), C.c_void_p()
+                _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(br), C.byref(a)))
+                self._ipc_mapped.append(a)
+                _native.check(L.tsb_ipc_open((C.c_uint8 * 64).from_buffer_copy(bf), C.byref(b)))
+                self._ipc_mapped.append(b)
+                pr[q], pf[q] = a, b
+        except Exception as exc:  # noqa: BLE001
+            ok, self.p2p_error = False, repr(exc)
+        if not self._agree(ok):  # (also orders every mapping before the first exchange)
+            return False
         _native.check(L.tsb_shard_p2p_set_peers(self._h, pr, pf))
+        return True
 
     @classmethod
     def from_network(cls, net, trips, config=None, seed=0, rank=0, nranks=1, device=0, group=None,

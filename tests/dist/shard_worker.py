@@ -61,6 +61,7 @@ def main():
         if bad:
             break
     ex = sw.exchanged_bytes
+    used_p2p = sw.p2p
     sw.close()
     ref.close()
     flag = np.array([bad])
@@ -68,7 +69,8 @@ def main():
     t = torch.tensor(flag)
     dist.all_reduce(t)
     if rank == 0:
-        print(f"SHARD_RESULT {name} ranks={ws} steps={steps} p2p={int(p2p)} mismatches={int(t.item())} "
+        print(f"SHARD_RESULT {name} ranks={ws} steps={steps} p2p={int(p2p)} p2p_used={int(used_p2p)} "
+              f"mismatches={int(t.item())} "
               f"bytes_rank0={ex}", flush=True)
     dist.destroy_process_group()
 

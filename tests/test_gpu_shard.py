@@ -12,15 +12,17 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(name, steps, nproc, port, mode=""):
+def _run(name, steps, nproc, port, mode="", env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "dist", "shard_worker.py"), name, str(steps)] + ([mode] if mode else [])
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=dict(os.environ, **(env or {})))
     line = [x for x in out.stdout.splitlines() if x.startswith("SHARD_RESULT")]
     assert line, out.stdout[-3000:] + out.stderr[-3000:]
     print(line[0])
     assert "mismatches=0" in line[0], out.stdout[-3000:]
+    return line[0]
 
 
 @pytest.mark.parametrize("name,steps,nproc,port", [("grid6x2", 300, 2, 29611), ("dense", 200, 2, 29612),
@@ -34,4 +36,11 @@ def test_sharded_p2p_equals_single(name, steps, nproc, port):
     """The device-driven exchange (pack into CUDA IPC-mapped peer slots,
     release/acquire flags, no host synchronisation per step), ranks sharing
     one GPU: same result as the single engine."""
-    _run(name, steps, nproc, port, "p2p")
+    assert "p2p_used=1" in _run(name, steps, nproc, port, "p2p")
+
+
+def test_sharded_p2p_fallback_when_a_rank_cannot_map():
+    """A rank that cannot map its peers makes every rank fall back to the
+    collective transport; results unchanged."""
+    line = _run("grid6x2", 60, 2, 29631, "p2p", env={"TSB_P2P_FAIL_RANK": "1"})
+    assert "p2p_used=0" in line
