@@ -36,6 +36,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 B_ALG = 60  # bytes per vehicle-update: r+w {id,lane,road_pos,s,v} + route gather
+# fp64 flops per vehicle-update in k_update (dadd + dmul + 2 x dfma thread
+# instructions of one launch / vehicles), from the ncu --set full capture
+FP64_FLOP_PER_UPDATE = 392.0
+FP64_FLOP_SOURCE = "ncu --set full of k_update<false> on M1 (profiles/r2a_k_update_ncu_summary.txt)"
 METRIC = "vehicle-updates/sec"
 UNIT = "vehicle-updates/s"
 
@@ -48,17 +52,51 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def build_workload(n_vehicles: int, spacing: float):
-    from paper_2405_12520_b200 import Router, generate_grid, preplaced_trips
+def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False):
+    """M1/C4 inputs.  oracle_router: routability from the CPU oracle's own
+    reverse Dijkstra (the reference arm never loads the product library);
+    otherwise the product's C++ Router.  Both give the same trips."""
+    from paper_2405_12520_b200 import generate_grid, preplaced_trips
     from paper_2405_12520_b200.flat import flatten_network, flatten_trips
 
     net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
     flat = flatten_network(net)
-    router = Router(net, flat=flat)
+    if oracle_router:
+        from oracle.bind import OracleRouter
+
+        router = OracleRouter(net, flat=flat)
+    else:
+        from paper_2405_12520_b200 import Router
+
+        router = Router(net, flat=flat)
     trips = preplaced_trips(net, router, n_vehicles, spacing)
     router.close()
     ft = flatten_trips(flat, trips)
     return net, flat, trips, ft
+
+
+def host_facts() -> dict:
+    """CPU model, threads, glibc and Python versions of the host."""
+    import ctypes
+    import platform
+
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        libc = ctypes.CDLL("libc.so.6")
+        libc.gnu_get_libc_version.restype = ctypes.c_char_p
+        glibc = libc.gnu_get_libc_version().decode()
+    except OSError:
+        glibc = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "glibc": glibc,
+            "python": platform.python_version(), "compiler": "gcc -O2 (oracle/Makefile)"}
 
 
 def run_sharded(args, ws, rank, local, pg, workload):
@@ -106,7 +144,7 @@ def run_sharded(args, ws, rank, local, pg, workload):
     hbm, peak_src = load_peaks()
     own = int((sw.plan.zone & 1).sum())
     halo = int(((sw.plan.zone & 2) > 0).sum())
-    xbytes = sw.exchanged_bytes
+    xbytes = sw.exchange_bytes()
     used_p2p, p2p_err = sw.p2p, sw.p2p_error
     sw.close()
     if rank != 0:
@@ -204,6 +242,42 @@ def cpu_baseline(net, flat, trips, warm: int, sample_steps: int, threads: int):
     return u / dt, u, dt
 
 
+TL_SLOTS, TL_ROWS = 16, 1024
+TL_PHASES = ("begin", "update", "scan", "place", "lanefix", "resolve_fast", "regroup", "end")
+
+
+def timeline_rows(L, h, n: int):
+    """The last n steps' %globaltimer stamps (ns) of the step timeline
+    (tsb_set_timeline), oldest first, as an (n, TL_SLOTS) int64 array."""
+    import numpy as np
+
+    from paper_2405_12520_b200 import _native
+
+    buf = np.zeros(TL_ROWS * TL_SLOTS, dtype=np.uint64)
+    _native.check(L.tsb_timeline(h, buf.ctypes.data))
+    t = buf.reshape(TL_ROWS, TL_SLOTS).astype(np.int64)
+    rows = t[t[:, 0] > 0]
+    rows = rows[np.argsort(rows[:, 0])]
+    return rows[-n:]
+
+
+def phase_durations(rows):
+    """In-graph duration (us) of each critical-path phase per step: from the
+    phase kernel passing its dependency wait to the next phase doing so
+    (k_update = scan start - update start).  Rows without a stamp (a phase
+    that did not run) are skipped per phase."""
+    import numpy as np
+
+    out = {}
+    for k in range(1, len(TL_PHASES) - 1):
+        a, b = rows[:, k], rows[:, k + 1]
+        ok = (a > 0) & (b > 0) & (b >= a)
+        if ok.any():
+            out[TL_PHASES[k]] = (b[ok] - a[ok]) / 1000.0
+    per = np.diff(rows[:, 0]) / 1000.0
+    return out, per
+
+
 def dist_setup():
     """torchrun environment -> (world size, rank, local rank, process group).
     TSB_BENCH_GLOO=1 (functional test on one GPU): gloo, every rank on cuda:0,
@@ -272,8 +346,8 @@ def path_counters(L, h):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--vehicles", type=int, default=1_000_000)
     ap.add_argument("--spacing", type=float, default=29.0)
@@ -300,22 +374,25 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
-        k = max(1, min(args.steps, args.cpu_sample_steps))
+        # the reference algorithm on the host: same workload, same K timed
+        # steps after the same W warm-up steps as the GPU arm (plus the
+        # excluded bulk-injection step); inputs built without the product
+        # library (routability from the oracle's own Dijkstra)
+        net, flat, trips, ft = build_workload(args.vehicles, args.spacing, oracle_router=True)
         cores = os.cpu_count() or 1
-        rate, u, dt = cpu_baseline(net, flat, trips, args.cpu_warm_steps, k, cores)
+        rate, u, dt = cpu_baseline(net, flat, trips, args.warmup, args.steps, cores)
         line = {
             "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": n_gpus,
-            "steps": k, "warmup": args.cpu_warm_steps, "ms_per_step": 1000.0 * dt / k,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload, "parallelism": f"cpu-{cores}-threads"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{k} steps x {args.vehicles} vehicles after injection + "
-                                       f"{args.cpu_warm_steps} warm-up steps (the revert regime the GPU arm is "
-                                       "timed in); "
+                             "sample": f"{args.steps} steps x {args.vehicles} vehicles after the bulk injection "
+                                       f"step + {args.warmup} warm-up steps, the GPU arm's window; "
                                        "oracle/oracle.c (C restatement of trafficsim World.step; the "
                                        f"reference is pure Python and cannot travel), update phase on {cores} "
-                                       "threads, commit phase sequential as in the reference"},
+                                       "threads, commit phase sequential as in the reference",
+                             "host": host_facts()},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line), flush=True)
@@ -326,6 +403,8 @@ def main():
         return
 
     import ctypes as C
+
+    import numpy as np
 
     from paper_2405_12520_b200 import EngineConfig, World
     from paper_2405_12520_b200 import _native
@@ -339,6 +418,13 @@ def main():
     if args.debug:
         _native.check(L.tsb_set_debug(world._h, args.debug))
     hbm, peak_src = load_peaks()
+    fp64_peak = C.c_double()
+    _native.check(L.tsb_fp64_peak(local, C.byref(fp64_peak)))
+    # step timeline on for the whole run: every step kernel's block 0 stamps
+    # %globaltimer; the in-graph kernel durations of the timed window come
+    # from it (one predicated store per kernel; the graph is rebuilt with it
+    # during the warm-up)
+    _native.check(L.tsb_set_timeline(world._h, 1))
     with ClockSampler(local) as clk:
         world.run(args.warmup)
         barrier(pg)
@@ -347,7 +433,7 @@ def main():
         ms = C.c_double()
         _native.check(L.tsb_time_steps(world._h, args.steps, C.byref(ms)))  # CUDA events, engine stream
         pc1 = path_counters(L, world._h)
-        world._report = world._report  # counters refreshed by tsb_time_steps' sync
+        rows = timeline_rows(L, world._h, args.steps)  # the K timed steps
         r = world._report
         _native.check(L.tsb_report_get(world._h, C.byref(r)))
         updates = r.vehicle_updates - u0
@@ -371,7 +457,9 @@ def main():
         _native.check(L.tsb_report_get(world._h, C.byref(world._report)))
         alt_rate = (world.vehicle_updates - u_alt0) / (ms_alt.value / 1e3)
         _native.check(L.tsb_set_pow_mode(world._h, pow_mode))
-        # per-kernel breakdown (separate pass, each kernel bracketed by events)
+        _native.check(L.tsb_set_timeline(world._h, 0))
+        # per-kernel breakdown, eager (each kernel bracketed by events,
+        # serialised): the launch list ncu sees, not the headline window
         kms = (C.c_double * 16)()
         nk = L.tsb_profile_steps(world._h, max(5, min(args.steps, 50)), 16, kms)
         if nk < 0:
@@ -381,22 +469,23 @@ def main():
     _native.check(L.tsb_report_get(world._h, C.byref(r_end)))
     launches = C.c_int32()
     _native.check(L.tsb_launches_per_step(world._h, C.byref(launches)))
+    sync_bytes = C.c_int64()
+    _native.check(L.tsb_step_sync_bytes(C.byref(sync_bytes)))
 
     t_max = allreduce_max(pg, ms.value)
     tot_updates = allreduce_sum(pg, float(updates))
     value = tot_updates / (t_max / 1e3)
     e2e_rate = allreduce_sum(pg, e2e_updates / e2e_dt)
     kernels = {L.tsb_kernel_name(k).decode(): kms[k] for k in range(nk)}
-    step_kernel_ms = sum(kernels.values())
-    top = max(kernels, key=kernels.get)
-    achieved = B_ALG * n_drv / (kernels[top] / 1e3) / 1e9  # GB/s, algorithmic bytes of one launch
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "k_update_dram.json")
-    if os.path.exists(prof_path):
-        try:
-            traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    # the dominant kernel in the headline window: in-graph durations from the
+    # step timeline of the K timed steps
+    ph, period = phase_durations(rows)
+    ph_mean = {k: float(np.mean(v)) for k, v in ph.items()}
+    top = "update"
+    k_us = ph_mean[top]
+    veh_per_launch = updates / args.steps
+    achieved = B_ALG * veh_per_launch / (k_us * 1e-6) / 1e9  # GB/s, algorithmic bytes of one launch
+    fp64_ach = FP64_FLOP_PER_UPDATE * veh_per_launch / (k_us * 1e-6) / 1e12
     world.close()
 
     cpu = None
@@ -408,7 +497,9 @@ def main():
                          f"injection + {args.cpu_warm_steps} warm-up steps (the revert regime the GPU arm is "
                          "timed in: the reference restarts its sweep after every revert); "
                          "oracle/oracle.c (C restatement of World.step), update "
-                         f"phase on {cores} threads, commit phase sequential as in the reference"}
+                         f"phase on {cores} threads, commit phase sequential as in the reference; "
+                         "bench.py --impl reference times the GPU arm's own K/W window",
+               "host": host_facts()}
     if rank != 0:
         return
     line = {
@@ -422,22 +513,37 @@ def main():
                    "timing": "CUDA events on the engine stream around K graph replays",
                    "pow": {"headline": args.pow, "value_pow_" + ("glibc" if pow_mode == 0 else "correct"): alt_rate,
                            "note": "correct = IDM powers correctly rounded (trajectories within 1e-12 m of the "
-                                   "reference, integer facts identical); glibc = glibc pow restated on the device, "
-                                   "record streams byte-identical to the reference (tests/test_gpu_golden.py)"},
+                                   "reference, integer facts identical; pinned at M1 by "
+                                   "tests/test_gpu_configs.py::test_m1_headline_arithmetic); glibc = glibc pow "
+                                   "restated on the device, record streams byte-identical to the reference "
+                                   "(tests/test_gpu_golden.py)"},
                    "reverts_per_step": r_end.reverts_total / max(1, r_end.step_no),
                    "paths_per_timed_step": {k: (pc1[i] - pc0[i]) / args.steps for i, k in enumerate(PATHS)},
                    "sequential_resolve_steps": r_end.resolve_sequential, "steps_total": r_end.step_no},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": C.sizeof(r),
-                "how": "World.step() loop (reference API), wall clock; each step syncs and copies its "
-                       "StepReport to the host; inputs were uploaded once at construction"},
+                "d2h_bytes_per_step": sync_bytes.value,
+                "how": "World.step() loop (reference API), wall clock; each step synchronises and reads the "
+                       "step scalars (StepReport counters + error flags) back to the host; a stateful "
+                       "simulator: inputs were uploaded once at construction, as the reference's bench "
+                       "(cli.py:482-489) times steps without a recorder"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "kernel": top,
+                     "frac": achieved / hbm, "traffic": None, "kernel": "k_update",
                      "peak_source": peak_src,
-                     "alg_bytes": f"{B_ALG} B/vehicle-update x {n_drv} vehicles per launch",
-                     "step_frac": B_ALG * value / n_gpus / 1e9 / hbm},
-        "kernel_ms_per_step": kernels,
-        "kernel_ms_sum": step_kernel_ms,
+                     "alg_bytes": f"{B_ALG} B/vehicle-update x {veh_per_launch:.0f} vehicles per launch",
+                     "duration_us": k_us,
+                     "duration_source": "in-graph, the K timed steps: %globaltimer stamps of k_update and of the "
+                                        "next kernel passing their dependency waits (tsb_set_timeline); CUDA "
+                                        "events cannot sit between PDL-chained graph kernel nodes",
+                     "traffic_note": "DRAM bytes per launch are in the ncu --set full capture under profiles/ "
+                                     "(not measurable inside this run)",
+                     "step_frac": B_ALG * value / n_gpus / 1e9 / hbm,
+                     "fp64": {"flop_per_update": FP64_FLOP_PER_UPDATE, "achieved_tflops": fp64_ach,
+                              "peak_tflops": fp64_peak.value, "frac": fp64_ach / fp64_peak.value,
+                              "flop_source": FP64_FLOP_SOURCE,
+                              "peak_source": "measured in this run (tsb_fp64_peak: DFMA chains, 2 flop each)"}},
+        "phases_us_in_graph": {k: round(v, 2) for k, v in ph_mean.items()},
+        "step_period_us_in_graph": float(np.mean(period)) if len(period) else None,
+        "eager_kernel_ms_per_step": kernels,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": launches.value * args.steps,

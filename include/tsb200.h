@@ -151,6 +151,13 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes);
 int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes);
 int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* peer_flags);
 int tsb_shard_p2p_exchange(tsb_engine* e);
+/* The device-side wait for a peer's arrival flag is bounded (default 60 s):
+ * on expiry the step completes with garbage ghosts and the next synchronising
+ * call returns TSB_ECUDA ("peer stopped stepping") instead of hanging. */
+int tsb_set_p2p_timeout(tsb_engine* e, double seconds);
+/* Bytes this rank's device-driven exchange wrote into its peers' receive
+ * slots since creation (per-lane count headers + 32 B records). */
+int tsb_exchange_bytes(tsb_engine* e, int64_t* out);
 /* cudaIpcGetMemHandle / cudaIpcOpenMemHandle / cudaIpcCloseMemHandle
  * (64-byte handles). */
 #define TSB_IPC_HANDLE_BYTES 64
@@ -236,14 +243,25 @@ int tsb_set_debug(tsb_engine* e, int32_t flags);
  * full regroups, out[4] steps that ran the injection section. */
 #define TSB_PATH_COUNTERS 5
 int tsb_path_counters(tsb_engine* e, int64_t* out);
-/* Step timeline (libraries built with -DTSB_TIMELINE, else TSB_EINVAL):
- * out[64 * 16] = %globaltimer stamps (ns) of the last 64 steps, a ring of
- * rows, slot = phase (kernels.cu TL_*), taken when the phase's kernel
- * passed its dependency wait. */
+/* Step timeline.  While on (tsb_set_timeline; turning it on clears the
+ * ring), every step kernel's block 0 stamps %globaltimer when it passed its
+ * dependency wait: out[TSB_TL_ROWS * TSB_TL_SLOTS] = stamps (ns) of the last
+ * TSB_TL_ROWS steps, a ring of rows, slot = phase (kernels.cu TL_*; 0 =
+ * step begin, 1 = k_update, 2 = lane scan, 7 = step end).  Used by bench.py
+ * for the in-graph kernel durations of the timed window. */
+#define TSB_TL_ROWS 1024
+#define TSB_TL_SLOTS 16
+int tsb_set_timeline(tsb_engine* e, int32_t on);
 int tsb_timeline(tsb_engine* e, uint64_t* out);
 /* Kernel launches every step issues (for the bench's gpu_launches claim):
  * the step graph's kernels outside its conditional (RARE) body. */
 int tsb_launches_per_step(tsb_engine* e, int32_t* n);
+/* Bytes a synchronising call (tsb_step, tsb_report_get) reads back from the
+ * device: the step scalars (StepReport counters, error flags). */
+int tsb_step_sync_bytes(int64_t* n);
+/* Measured fp64 FMA throughput of a device (TFLOP/s, 2 flops per DFMA):
+ * the denominator bench.py reports k_update's fp64 rate against. */
+int tsb_fp64_peak(int32_t device, double* tflops);
 
 #ifdef __cplusplus
 }

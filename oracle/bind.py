@@ -53,10 +53,30 @@ def lib():
         L.orc_keyed_uniform4.argtypes = [C.c_uint64] * 4
         L.orc_keyed_uniform4.restype = C.c_double
         L.orc_set_threads.argtypes = [vp, C.c_int32]
+        L.orc_reach.argtypes = [vp, C.c_int32, vp, vp]
         L.orc_pow_cr.argtypes = [C.c_double, C.c_int32]
         L.orc_pow_cr.restype = C.c_double
         _LIB = L
     return _LIB
+
+
+class OracleRouter:
+    """Router.dist_to key sets from the oracle's own reverse Dijkstra
+    (routing.py:47-68), for building demand without the product library
+    (bench.py's CPU arm).  Same interface as Router.reachable_sets."""
+
+    def __init__(self, net, config: EngineConfig | None = None, flat=None):
+        self._w = OracleWorld(net, [], config, flat=flat)
+        self._n = self._w.flat.n_lanes
+
+    def reachable_sets(self, dests) -> dict:
+        d = np.asarray(dests, dtype=np.int32)
+        out = np.zeros((len(d), max(self._n, 1)), dtype=np.uint8)
+        lib().orc_reach(self._w._h, len(d), d.ctypes.data, out.ctypes.data)
+        return {int(k): out[i].astype(bool) for i, k in enumerate(d)}
+
+    def close(self):
+        self._w.close()
 
 
 class OracleWorld:

@@ -1232,6 +1232,21 @@ int orc_route_cost(orc* o, int32_t origin, int32_t dest, double* cost, int32_t* 
   return OK;
 }
 
+/* Router.dist_to(dest) key sets for n destinations (routing.py:47-68: an
+ * origin can reach dest iff it is a key of dist_to(dest)); out is n x lanes. */
+int orc_reach(orc* o, int32_t n, const int32_t* dests, uint8_t* out) {
+  for (int32_t i = 0; i < n; i++) {
+    uint8_t* row = out + (size_t)i * (size_t)o->nl;
+    if (o->w[dests[i]] < 0) {
+      memset(row, 0, (size_t)o->nl);
+      continue;
+    }
+    const double* dist = dist_to(o, dests[i]);
+    for (int32_t l = 0; l < o->nl; l++) row[l] = dist[l] >= 0;
+  }
+  return OK;
+}
+
 /* Threads for the update phase (EngineConfig.threads, params.py:48-83). */
 int orc_set_threads(orc* o, int32_t n) {
   o->threads = n < 1 ? 1 : n;

@@ -48,6 +48,9 @@ SIGNATURES = {
     "tsb_set_debug": (_i32, [_vp, _i32]),
     "tsb_path_counters": (_i32, [_vp, _vp]),
     "tsb_timeline": (_i32, [_vp, _vp]),
+    "tsb_set_timeline": (_i32, [_vp, _i32]),
+    "tsb_fp64_peak": (_i32, [_i32, C.POINTER(_f64)]),
+    "tsb_step_sync_bytes": (_i32, [C.POINTER(_i64)]),
     "tsb_create_sharded": (_i32, [_vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
     "tsb_mark": (_i32, [_vp, _i32]),
     "tsb_set_pow_mode": (_i32, [_vp, _i32]),
@@ -57,6 +60,8 @@ SIGNATURES = {
     "tsb_shard_p2p_alloc": (_i32, [_vp, _vp, _vp, _vp]),
     "tsb_shard_p2p_set_peers": (_i32, [_vp, _vp, _vp]),
     "tsb_shard_p2p_exchange": (_i32, [_vp]),
+    "tsb_set_p2p_timeout": (_i32, [_vp, _f64]),
+    "tsb_exchange_bytes": (_i32, [_vp, C.POINTER(_i64)]),
     "tsb_step_async": (_i32, [_vp, _i32]),
     "tsb_ipc_handle": (_i32, [_vp, _vp]),
     "tsb_ipc_open": (_i32, [_vp, _vp]),

@@ -124,10 +124,11 @@ struct Dyn {
   int32_t rf_done;      // k_resolve_fast replayed every event
   int32_t rg_done;      // k_regroup: blocks finished (the last one ends the step)
   int32_t rf_fin;       // k_resolve_fast: replays finished
-  int32_t tl_row;       // TSB_TIMELINE builds: the step's row in the timeline ring
+  int32_t tl_row;       // the step's row in the timeline ring (while the timeline is on)
   int32_t rare;         // the step takes the RARE body (set_rare)
   int32_t pad4_;
   unsigned long long xchg_epoch;  // sharded P2P exchanges so far (k_exp_count)
+  unsigned long long xchg_bytes;  // sharded P2P: bytes this rank wrote into peer slots so far
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };
@@ -217,6 +218,7 @@ struct Ctx {
   unsigned long long* p2p_peer_flag[8];
   unsigned long long* p2p_flag;  // own flags [parity][source rank]
   int64_t p2p_slot;               // bytes per slot
+  uint64_t p2p_timeout_ns;        // k_p2p_wait gives up after this long (overflow bit 0x80)
   int32_t* comp_flags;  // per component: bit 0 has an own lane, bit 1 has an inexact lane
   // conditional sections of the step graph (kernels.cu set_cond)
   unsigned long long cond[4];
@@ -272,7 +274,8 @@ struct Ctx {
   int32_t n_win;
   int32_t* hostq;
   Dyn* dyn;
-  unsigned long long* tl;  // TSB_TIMELINE builds: 64 x 16 step timestamps
+  unsigned long long* tl;  // step timestamps, TL_ROWS x TL_SLOTS (kernels.cu TL_MARK)
+  int32_t tl_on;           // tsb_set_timeline
   double* scratch_d;
 };
 

@@ -391,10 +391,14 @@ static int flush_speeds(tsb_engine* e) {
 static int sync_dyn(tsb_engine* e) {
   CK(cudaMemcpyAsync(e->dyn_host, e->c.dyn, sizeof(Dyn), cudaMemcpyDeviceToHost, e->stream));
   CK(cudaStreamSynchronize(e->stream));
+  if (e->dyn_host->overflow & 128)
+    return fail(TSB_ECUDA, "sharded exchange: a peer's arrival flag did not come within %.3f s (peer stopped stepping?)",
+                1e-9 * (double)e->c.p2p_timeout_ns);
   if (e->dyn_host->overflow)
     return fail(TSB_ECAP,
                 "engine capacity/consistency flag 0x%x set (0x2 speed windows, 0x4 host reroute outside split mode, "
-                "0x10 a sharded revert chain left the exact zone, 0x20 regroup path, 0x40 ghost capacity)",
+                "0x10 a sharded revert chain left the exact zone, 0x20 regroup path, 0x40 ghost capacity, "
+                "0x80 a peer's exchange flag did not arrive within the P2P timeout)",
                 e->dyn_host->overflow);
   return TSB_OK;
 }
@@ -771,7 +775,12 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   if (sh && p->controller != 0) return fail(TSB_EINVAL, "sharded mode supports fixed-time signals only");
   if (p->pow_mode != 0 && p->pow_mode != 1)
     return fail(TSB_EINVAL, "pow_mode %d unsupported (0 = correctly rounded, 1 = glibc pow)", p->pow_mode);
-  auto e = std::make_unique<tsb_engine>();
+  // an early error return destroys the partly built engine (streams, events,
+  // allocations) through tsb_destroy
+  struct Destroy {
+    void operator()(tsb_engine* x) const { tsb_destroy(x); }
+  };
+  std::unique_ptr<tsb_engine, Destroy> e(new tsb_engine());
   e->device = device;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
@@ -791,6 +800,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
   e->cur = e->stream;
+  e->c.p2p_timeout_ns = 60ULL * 1000000000ULL;
   const int32_t NL = e->n_lanes = net->n_lanes;
   const int32_t NR = e->n_roads = net->n_roads;
   const int32_t NJ = e->n_junc = net->n_junctions;
@@ -1036,7 +1046,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.rs_touched, NL));
   RC(dalloc(E, &c.rs_event, NL));
   RC(dalloc(E, &c.rf_owner, NL));
-  RC(dalloc(E, &c.tl, 64 * 16));
+  RC(dalloc(E, &c.tl, (size_t)TL_ROWS * TL_SLOTS));
   RC(dalloc(E, &c.rs_movedin, NL));
   RC(dalloc(E, &c.rs_moved, CAP));
   RC(dalloc(E, &c.rs_reverted, CAP));
@@ -1155,7 +1165,10 @@ int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_
     e->allocs.push_back(r);
     CK(cudaMalloc((void**)&f, sizeof(unsigned long long) * 2 * c.nranks));
     e->allocs.push_back(f);
-    CK(cudaMemset(f, 0, sizeof(unsigned long long) * 2 * c.nranks));
+    // cleared on the engine stream and completed before the handles are
+    // published: no peer can signal into a flag word a late memset would erase
+    CK(cudaMemsetAsync(f, 0, sizeof(unsigned long long) * 2 * c.nranks, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
     e->p2p_recv = r;
     c.p2p_flag = f;
   }
@@ -1197,6 +1210,22 @@ int tsb_shard_p2p_set_peers(tsb_engine* e, void* const* peer_recv, void* const* 
   return TSB_OK;
 }
 
+int tsb_exchange_bytes(tsb_engine* e, int64_t* out) {
+  if (!e || !out) return fail(TSB_EINVAL, "null argument");
+  CK(cudaSetDevice(e->device));
+  RC(sync_dyn(e));
+  *out = (int64_t)e->dyn_host->xchg_bytes;
+  return TSB_OK;
+}
+
+int tsb_set_p2p_timeout(tsb_engine* e, double seconds) {
+  if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
+  if (!(seconds > 0.0) || seconds > 1e6) return fail(TSB_EINVAL, "timeout must be in (0, 1e6] s");
+  e->c.p2p_timeout_ns = (uint64_t)(seconds * 1e9);
+  e->graph_dirty = true;  // Ctx is captured by value in the step graph
+  return TSB_OK;
+}
+
 int tsb_shard_p2p_exchange(tsb_engine* e) {
   if (!e || !e->c.sharded || !e->p2p_ready) return fail(TSB_EINVAL, "P2P exchange not set up");
   Launcher L{e};
@@ -1220,6 +1249,9 @@ void tsb_destroy(tsb_engine* e) {
   if (e->body) cudaStreamDestroy(e->body);
   if (e->side) cudaStreamDestroy(e->side);
   if (e->side2) cudaStreamDestroy(e->side2);
+  if (e->side3) cudaStreamDestroy(e->side3);
+  if (e->ev_fork3) cudaEventDestroy(e->ev_fork3);
+  if (e->ev_join3) cudaEventDestroy(e->ev_join3);
   if (e->ev_fork2) cudaEventDestroy(e->ev_fork2);
   if (e->ev_join2) cudaEventDestroy(e->ev_join2);
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
@@ -1521,16 +1553,22 @@ int tsb_set_debug(tsb_engine* e, int32_t flags) {
   return TSB_OK;
 }
 
-int tsb_timeline(tsb_engine* e, uint64_t* out) {
-#ifdef TSB_TIMELINE
-  RC(sync_dyn(e));
-  CK(cudaMemcpy(out, e->c.tl, sizeof(uint64_t) * 64 * 16, cudaMemcpyDeviceToHost));
+int tsb_set_timeline(tsb_engine* e, int32_t on) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  CK(cudaSetDevice(e->device));
+  if (on && !e->c.tl_on) {  // a fresh ring: rows of earlier windows never mix in
+    CK(cudaMemsetAsync(e->c.tl, 0, sizeof(uint64_t) * TL_ROWS * TL_SLOTS, e->stream));
+  }
+  e->c.tl_on = on ? 1 : 0;
+  e->graph_dirty = true;  // Ctx is captured by value in the step graph
   return TSB_OK;
-#else
-  (void)e;
-  (void)out;
-  return fail(TSB_EINVAL, "library built without -DTSB_TIMELINE");
-#endif
+}
+
+int tsb_timeline(tsb_engine* e, uint64_t* out) {
+  if (!e || !out) return fail(TSB_EINVAL, "null argument");
+  RC(sync_dyn(e));
+  CK(cudaMemcpy(out, e->c.tl, sizeof(uint64_t) * TL_ROWS * TL_SLOTS, cudaMemcpyDeviceToHost));
+  return TSB_OK;
 }
 
 int tsb_path_counters(tsb_engine* e, int64_t* out) {
@@ -1539,6 +1577,56 @@ int tsb_path_counters(tsb_engine* e, int64_t* out) {
   const int64_t v[TSB_PATH_COUNTERS] = {d.n_resolve_fast, d.n_resolve_general, d.n_regroup_patch,
                                         d.n_regroup_full, d.n_inject_steps};
   for (int k = 0; k < TSB_PATH_COUNTERS; k++) out[k] = v[k];
+  return TSB_OK;
+}
+
+// fp64 FMA throughput of the device (the denominator of k_update's fp64
+// fraction in bench.py): every thread runs 8 independent DFMA chains.
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int k = 0; k < iters; k++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (r == 12345.678) out[0] = r;  // keeps the chains alive
+}
+
+int tsb_fp64_peak(int32_t device, double* tflops) {
+  if (!tflops) return fail(TSB_EINVAL, "null argument");
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* out = nullptr;
+  CK(cudaMalloc((void**)&out, sizeof(double)));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int threads = 256, blocks = sms * 8, iters = 2048;
+  float best = 1e30f;
+  for (int rep = 0; rep < 6; rep++) {
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0 && ms < best) best = ms;  // the first launch warms up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * 8.0 * (double)iters * (double)threads * (double)blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return TSB_OK;
+}
+
+int tsb_step_sync_bytes(int64_t* n) {
+  if (!n) return fail(TSB_EINVAL, "null argument");
+  *n = (int64_t)sizeof(Dyn);
   return TSB_OK;
 }
 

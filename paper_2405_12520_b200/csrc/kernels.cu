@@ -39,26 +39,24 @@ static constexpr double EPS_GAP = 1e-6;  // world.py:43
 // grid (and its memory) before anything is read.  No-op without the attribute.
 #define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 
-// Step timeline (measurement builds, -DTSB_TIMELINE): block 0 of a kernel
-// stamps %globaltimer once its predecessors completed (after PDL_WAIT), into
-// slot k of the current step's row of c.tl (64 steps x TL_SLOTS, a ring).
+// Step timeline (tsb_set_timeline): while c.tl_on, block 0 of each step
+// kernel stamps %globaltimer once its predecessors completed (after
+// PDL_WAIT), into slot k of the current step's row of c.tl (a ring of
+// TL_ROWS steps x TL_SLOTS).  bench.py reads the in-graph duration of
+// k_update from it over the timed window itself; one load and a predicated
+// store per kernel when off.
 static constexpr int TL_SLOTS = 16;
+static constexpr int TL_ROWS = 1024;
 enum { TL_BEGIN, TL_UPDATE, TL_SCAN, TL_PLACE, TL_LANEFIX, TL_RESOLVE, TL_REGROUP, TL_END, TL_SPEEDS, TL_SIGNALS,
        TL_INJECT_DUE, TL_SPEEDS_END };
-#ifdef TSB_TIMELINE
 #define TL_MARK(k)                                                                        \
   do {                                                                                    \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {                                            \
+    if (c.tl_on && blockIdx.x == 0 && threadIdx.x == 0) {                                 \
       unsigned long long t_;                                                              \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
-      c.tl[(size_t)(c.dyn->tl_row & 63) * TL_SLOTS + (k)] = t_;                           \
+      c.tl[(size_t)(c.dyn->tl_row & (TL_ROWS - 1)) * TL_SLOTS + (k)] = t_;                \
     }                                                                                     \
   } while (0)
-#else
-#define TL_MARK(k) \
-  do {             \
-  } while (0)
-#endif
 
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
@@ -1903,6 +1901,8 @@ __device__ void rf_writeback(const Ctx& c, VRec* C, const RfE* E, int32_t ncache
 // RARE body of the step graph.  The warps of one launch wait for each other once
 // (all co-resident: at most RF_BLOCKS small blocks).
 static constexpr int RF_BLOCKS = 64;
+static constexpr int32_t RF_ABORT = 1 << 30;                // k_resolve_fast arrival word: wait aborted
+static constexpr unsigned long long RF_WAIT_NS = 2000000ULL;  // 2 ms (the wait takes microseconds)
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_RESOLVE);
@@ -2030,12 +2030,29 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
 #endif
   if (lid == 0) {
+    // Launch-wide wait, bounded: the launch is not cooperative, so its blocks
+    // are co-resident only in practice (a shared or MPS-partitioned GPU may
+    // delay some).  A warp that waits longer than RF_WAIT_NS aborts the fast
+    // path for the whole launch by setting RF_ABORT in the arrival word, but
+    // only while the count is short of ne (a CAS on the observed word): the
+    // warps either all see every arrival without the bit (fast path) or all
+    // see the bit (general path).  Nothing global was modified before this
+    // point except the epoch-tagged lane claims.
     if (bad) atomicExch(&dy->rf_conflict, 1);
     __threadfence();
-    atomicAdd(&dy->rf_arrive, 1);
-    while (atomicAdd(&dy->rf_arrive, 0) < ne) __nanosleep(64);
+    int32_t a = atomicAdd(&dy->rf_arrive, 1) + 1;
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    while (!(a & RF_ABORT) && a < ne) {
+      __nanosleep(64);
+      a = atomicAdd(&dy->rf_arrive, 0);
+      if (a & RF_ABORT || a >= ne) break;
+      unsigned long long t_now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+      if (t_now - t_start > RF_WAIT_NS) a = atomicCAS(&dy->rf_arrive, a, a | RF_ABORT) == a ? (a | RF_ABORT) : a;
+    }
     __threadfence();
-    s_bad[w] = atomicAdd(&dy->rf_conflict, 0);
+    s_bad[w] = (a & RF_ABORT) ? 1 : atomicAdd(&dy->rf_conflict, 0);
   }
   __syncwarp();
   if (s_bad[w]) {
@@ -2564,13 +2581,11 @@ __global__ void __launch_bounds__(32 * PD_WARPS) k_regroup(Ctx c, int may_full) 
   if (!s_last) return;
   __threadfence();
   regroup_finish(c);
-#ifdef TSB_TIMELINE
-  if (threadIdx.x == 0) {
+  if (c.tl_on && threadIdx.x == 0) {
     unsigned long long t_;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
-    c.tl[(size_t)(c.dyn->tl_row & 63) * TL_SLOTS + TL_END] = t_;
+    c.tl[(size_t)(c.dyn->tl_row & (TL_ROWS - 1)) * TL_SLOTS + TL_END] = t_;
   }
-#endif
 }
 
 // End of a step whose snapshot the full regroup rebuilt.
@@ -2631,10 +2646,8 @@ __global__ void k_begin_step(Ctx c) {
   PDL_WAIT();
   for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) c.cnt[L] = 0;
   if (gtid() != 0) return;
-#ifdef TSB_TIMELINE
-  c.dyn->tl_row += 1;
+  if (c.tl_on) c.dyn->tl_row += 1;
   TL_MARK(TL_BEGIN);
-#endif
   Dyn* dy = c.dyn;
   dy->vehicle_updates += c.sharded ? dy->n_own : dy->n_drv;
   dy->finished_now = 0;
@@ -2777,6 +2790,7 @@ __global__ void k_exp_pack_p2p(Ctx c) {
   const int2* S = c.rng[c.dyn->cur];
   const int lid = threadIdx.x & 31;
   const int64_t slot = (int64_t)((epoch & 1) * c.nranks + c.rank) * c.p2p_slot;
+  if (gtid() == 0) c.dyn->xchg_bytes += (unsigned long long)exp_base(c, c.nranks);  // every peer's message
   for (int32_t e = gtid() >> 5; e < c.n_exp; e += gstride() >> 5) {
     const int q = c.exp_peer[e];
     const int64_t e0 = c.peer_first_exp[q];
@@ -2807,11 +2821,17 @@ __global__ void k_p2p_wait(Ctx c) {
   const int q = threadIdx.x;
   if (q < c.nranks && q != c.rank) {
     const unsigned long long* f = c.p2p_flag + (epoch & 1) * c.nranks + q;
-    unsigned long long v;
+    unsigned long long v, t_start, t_now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
       if (v >= epoch) break;
       __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+      if (t_now - t_start > c.p2p_timeout_ns) {  // a peer stopped stepping: fail loudly, do not hang
+        atomicOr(&c.dyn->overflow, 128);
+        break;
+      }
     }
   }
   __syncthreads();

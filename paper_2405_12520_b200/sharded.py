@@ -113,14 +113,6 @@ class ShardedWorld:
             self.p2p = self._setup_p2p()
         self._exchange()  # initial ghosts (empty network: zero vehicles)
 
-    def _agree(self, ok: bool) -> bool:
-        """True iff every rank says ok (one all-reduce, every rank calls)."""
-        t = self.torch.tensor([1 if ok else 0], dtype=self.torch.int64)
-        if not self.host_staging:
-            t = t.to(self.device)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
-        return bool(int(t.item()))
-
     def _setup_p2p(self) -> bool:
         """Receive slots and arrival flags of every rank mapped into every
         other rank (CUDA IPC handles exchanged once through the process
@@ -142,12 +134,13 @@ class ShardedWorld:
         except Exception as exc:  # noqa: BLE001 -- reported, then the fallback
             ok, self.p2p_error = False, repr(exc)
         got = [None] * self.nranks
-        self.dist.all_gather_object(got, (ok, bytes(hr), bytes(hf)), group=self.group)
+        self.dist.all_gather_object(got, (ok, bytes(hr), bytes(hf), self.p2p_error), group=self.group)
         if not all(g[0] for g in got):
+            self.p2p_error = "; ".join(f"rank {q}: {g[3]}" for q, g in enumerate(got) if not g[0])
             return False
         pr, pf = (C.c_void_p * self.nranks)(), (C.c_void_p * self.nranks)()
         try:
-            for q, (_, br, bf) in enumerate(got):
+            for q, (_, br, bf, _) in enumerate(got):
                 if q == self.rank:
                     pr[q], pf[q] = recv, flags
                     continue
@@ -159,7 +152,10 @@ class ShardedWorld:
                 pr[q], pf[q] = a, b
         except Exception as exc:  # noqa: BLE001
             ok, self.p2p_error = False, repr(exc)
-        if not self._agree(ok):  # (also orders every mapping before the first exchange)
+        errs = [None] * self.nranks  # (also orders every mapping before the first exchange)
+        self.dist.all_gather_object(errs, (ok, self.p2p_error), group=self.group)
+        if not all(g[0] for g in errs):
+            self.p2p_error = "; ".join(f"rank {q}: {g[1]}" for q, g in enumerate(errs) if not g[0])
             return False
         _native.check(L.tsb_shard_p2p_set_peers(self._h, pr, pf))
         return True
@@ -212,6 +208,18 @@ class ShardedWorld:
         for _ in range(n):
             _native.check(_native.lib().tsb_step(self._h, 1, C.byref(self._report)))
             self._exchange()
+
+    def exchange_bytes(self) -> int:
+        """Bytes this rank sent to its peers so far (either transport)."""
+        if self.p2p:
+            out = C.c_int64()
+            _native.check(_native.lib().tsb_exchange_bytes(self._h, C.byref(out)))
+            return int(out.value)
+        return self.exchanged_bytes
+
+    def set_p2p_timeout(self, seconds: float) -> None:
+        """Bound of the device-side wait for a peer's step (TSB_ECUDA on expiry)."""
+        _native.check(_native.lib().tsb_set_p2p_timeout(self._h, float(seconds)))
 
     def report(self) -> dict:
         """StepReport counters summed over ranks (time and step are shared)."""

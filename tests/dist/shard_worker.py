@@ -27,13 +27,67 @@ SCEN = {
 }
 
 
+def scenario(name):
+    """(net, trips, seed) of a named scenario; "m1" is bench.py's workload
+    (100x100x3 grid, 1M pre-placed routable vehicles)."""
+    if name == "m1":
+        from paper_2405_12520_b200 import Router, preplaced_trips
+
+        net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
+        router = Router(net)
+        trips = preplaced_trips(net, router, 1_000_000, 29.0)
+        router.close()
+        return net, trips, 42
+    net, n, seed, window = SCEN[name]()
+    return net, random_trips(net, n, seed=seed, window=window), seed
+
+
+def agree_bad(bad: int) -> int:
+    """Mismatch count summed over ranks: every rank stops at the same step
+    (a rank-local break would leave its peers waiting in a collective)."""
+    import torch
+
+    t = torch.tensor([bad])
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def stall_test():
+    """Rank 1 stops stepping; rank 0's bounded device-side wait for rank 1's
+    exchange flag must end the step with TSB_ECUDA (EngineError), not hang."""
+    from paper_2405_12520_b200.errors import EngineError
+
+    rank, ws = dist.get_rank(), dist.get_world_size()
+    net, trips, seed = scenario("grid6x2")
+    sw = ShardedWorld.from_network(net, trips, EngineConfig(), seed=seed, rank=rank, nranks=ws, device=0,
+                                   host_staging=True, p2p=True)
+    assert sw.p2p, sw.p2p_error
+    sw.set_p2p_timeout(0.5)
+    sw.step_local(5)
+    dist.barrier()
+    msg = "no error"
+    if rank == 0:
+        try:
+            sw.step_local(3)  # rank 1 is not stepping
+        except EngineError as exc:
+            msg = str(exc)
+    dist.barrier()
+    sw.close()
+    if rank == 0:
+        ok = "did not come within" in msg
+        print(f"STALL_RESULT ok={int(ok)} msg={msg!r}", flush=True)
+
+
 def main():
     name, steps = sys.argv[1], int(sys.argv[2])
     p2p = len(sys.argv) > 3 and sys.argv[3] == "p2p"
     dist.init_process_group("gloo")
+    if name == "stall":
+        stall_test()
+        dist.destroy_process_group()
+        return
     rank, ws = dist.get_rank(), dist.get_world_size()
-    net, n, seed, window = SCEN[name]()
-    trips = random_trips(net, n, seed=seed, window=window)
+    net, trips, seed = scenario(name)
     cfg = EngineConfig()
     sw = ShardedWorld.from_network(net, trips, cfg, seed=seed, rank=rank, nranks=ws, device=0, host_staging=True,
                                    p2p=p2p)
@@ -58,19 +112,16 @@ def main():
                     print(f"rank {rank} step {k}: own-lane field {key} differs", flush=True)
                     bad += 1
                     break
-        if bad:
+        if agree_bad(bad):
             break
-    ex = sw.exchanged_bytes
+    ex = sw.exchange_bytes()
     used_p2p = sw.p2p
     sw.close()
     ref.close()
-    flag = np.array([bad])
-    import torch
-    t = torch.tensor(flag)
-    dist.all_reduce(t)
+    total_bad = agree_bad(bad)
     if rank == 0:
         print(f"SHARD_RESULT {name} ranks={ws} steps={steps} p2p={int(p2p)} p2p_used={int(used_p2p)} "
-              f"mismatches={int(t.item())} "
+              f"mismatches={total_bad} "
               f"bytes_rank0={ex}", flush=True)
     dist.destroy_process_group()
 

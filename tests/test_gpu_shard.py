@@ -12,12 +12,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(name, steps, nproc, port, mode="", env=None):
+def _launch(name, steps, nproc, port, mode="", env=None, timeout=600):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "dist", "shard_worker.py"), name, str(steps)] + ([mode] if mode else [])
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                         env=dict(os.environ, **(env or {})))
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                          env=dict(os.environ, **(env or {})))
+
+
+def _run(name, steps, nproc, port, mode="", env=None, timeout=600):
+    out = _launch(name, steps, nproc, port, mode, env, timeout)
     line = [x for x in out.stdout.splitlines() if x.startswith("SHARD_RESULT")]
     assert line, out.stdout[-3000:] + out.stderr[-3000:]
     print(line[0])
@@ -44,3 +48,20 @@ def test_sharded_p2p_fallback_when_a_rank_cannot_map():
     collective transport; results unchanged."""
     line = _run("grid6x2", 60, 2, 29631, "p2p", env={"TSB_P2P_FAIL_RANK": "1"})
     assert "p2p_used=0" in line
+
+
+def test_sharded_m1_two_ranks_p2p():
+    """The bench workload (M1: 100x100x3 grid, 1M vehicles) split into 2 lane
+    bands, ranks sharing one GPU, device-driven exchange: every StepReport
+    counter summed over ranks each step and every rank's own lanes bit for bit
+    against the single engine, 10 steps (the bulk injection included)."""
+    assert "p2p_used=1" in _run("m1", 10, 2, 29641, "p2p", timeout=1200)
+
+
+def test_sharded_p2p_peer_stall_fails_loudly():
+    """A rank that stops stepping: its peer's bounded device-side wait ends
+    the step and the engine raises EngineError (TSB_ECUDA) instead of hanging."""
+    out = _launch("stall", 0, 2, 29651, timeout=300)
+    line = [x for x in out.stdout.splitlines() if x.startswith("STALL_RESULT")]
+    assert line, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "ok=1" in line[0], line[0]
