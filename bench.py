@@ -53,26 +53,37 @@ def load_peaks():
 
 
 def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False):
-    """M1/C4 inputs.  oracle_router: routability from the CPU oracle's own
-    reverse Dijkstra (the reference arm never loads the product library);
-    otherwise the product's C++ Router.  Both give the same trips."""
-    from paper_2405_12520_b200 import generate_grid, preplaced_trips
+    """M1/C4 inputs -> (net or None, FlatNet, trips, FlatTrips, junction positions).
+
+    GPU arm: the native grid builder (csrc/gridgen.cpp, pinned by sha256 to
+    the reference's generate_grid at this size) and the product's C++ Router.
+    Reference arm (oracle_router): the Python builders and the CPU oracle's own
+    reverse Dijkstra -- that process never loads the product library.  Both
+    give the same network and the same trips."""
+    import numpy as np
+
+    from paper_2405_12520_b200 import preplaced_trips
     from paper_2405_12520_b200.flat import flatten_network, flatten_trips
 
-    net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
-    flat = flatten_network(net)
     if oracle_router:
         from oracle.bind import OracleRouter
+        from paper_2405_12520_b200 import generate_grid
 
+        net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
+        flat = flatten_network(net)
+        jpos = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
         router = OracleRouter(net, flat=flat)
     else:
         from paper_2405_12520_b200 import Router
+        from paper_2405_12520_b200.gridgen import grid_flat
 
-        router = Router(net, flat=flat)
-    trips = preplaced_trips(net, router, n_vehicles, spacing)
+        net = None
+        flat, jpos = grid_flat(100, 100, block_length=400.0, lanes_per_direction=3)
+        router = Router(None, flat=flat)
+    trips = preplaced_trips(flat if net is None else net, router, n_vehicles, spacing)
     router.close()
     ft = flatten_trips(flat, trips)
-    return net, flat, trips, ft
+    return net, flat, trips, ft, jpos
 
 
 def host_facts() -> dict:
@@ -109,8 +120,7 @@ def run_sharded(args, ws, rank, local, pg, workload):
     from paper_2405_12520_b200 import EngineConfig, _native
     from paper_2405_12520_b200.sharded import ShardedWorld
 
-    net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
-    jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    net, flat, trips, ft, jp = build_workload(args.vehicles, args.spacing)
     p2p = args.exchange == "p2p"
     sw = ShardedWorld(flat, ft, jp, EngineConfig(), 42, rank, ws, device=local,
                       host_staging=os.environ.get("TSB_BENCH_GLOO") == "1", p2p=p2p)
@@ -378,7 +388,7 @@ def main():
         # steps after the same W warm-up steps as the GPU arm (plus the
         # excluded bulk-injection step); inputs built without the product
         # library (routability from the oracle's own Dijkstra)
-        net, flat, trips, ft = build_workload(args.vehicles, args.spacing, oracle_router=True)
+        net, flat, trips, ft, _ = build_workload(args.vehicles, args.spacing, oracle_router=True)
         cores = os.cpu_count() or 1
         rate, u, dt = cpu_baseline(net, flat, trips, args.warmup, args.steps, cores)
         line = {
@@ -409,7 +419,7 @@ def main():
     from paper_2405_12520_b200 import EngineConfig, World
     from paper_2405_12520_b200 import _native
 
-    net, flat, trips, ft = build_workload(args.vehicles, args.spacing)
+    net, flat, trips, ft, _ = build_workload(args.vehicles, args.spacing)
     pow_mode = 1 if args.pow == "glibc" else 0
     world = World.from_flat(flat, ft, EngineConfig(), seed=42, device=local, pow_mode=pow_mode)
     world.step()  # bulk injection of all pre-placed vehicles (excluded)

@@ -196,6 +196,40 @@ int tsb_road_acc(tsb_engine* e, int32_t n_windows, double* sum, int64_t* count);
 /* World.min_front_gap (world.py:694-704), computed on device. */
 int tsb_min_front_gap(tsb_engine* e, double* out);
 
+/* Per-id query: World.get_vehicle -> StatusView (world.py:83-92, 706-714),
+ * answered on the device for just the requested vehicles (a locator kernel
+ * maps vix -> snapshot record, then one gather per query).
+ * status: TSB_STATUS_*; driving: the snapshot state (world.py:712); finished:
+ * the last committed state before arrival (world.py:488-494) and finish_time;
+ * waiting/dropped: origin lane and s, v = 0, road_pos = 0.  A sharded engine
+ * reports TSB_STATUS_ELSEWHERE for a vehicle driving on another rank's lanes. */
+#define TSB_STATUS_ELSEWHERE (-1)
+typedef struct tsb_vehicle_view {
+  double s, v;
+  double finish_time; /* finished vehicles only */
+  int32_t lane;
+  int32_t road_pos;   /* roads_seq index; route_index = 2*road_pos + (lane is a connector) */
+  int32_t status;
+  int32_t pad;
+} tsb_vehicle_view;
+int tsb_get_vehicles(tsb_engine* e, const int32_t* vix, int32_t n, tsb_vehicle_view* out);
+
+/* Lane geometry for record angles (geometry.py:22-52): per lane, the
+ * centerline segments [geo_off[l], geo_off[l+1]), each with its start arc
+ * position geo_cum[k] and its heading geo_angle[k] in degrees (evaluated on
+ * the host with the reference's own expression: math.degrees(atan2(dx, dy))
+ * % 360).  Copied to the device; required before tsb_records. */
+int tsb_set_geometry(tsb_engine* e, const int64_t* geo_off, int64_t n_segments, const double* geo_cum,
+                     const double* geo_angle);
+/* World.record_step (world.py:771-782) as a batch: every driving vehicle of
+ * the snapshot (a sharded engine: of its own lanes) in ascending id (vix)
+ * order, with its heading at min(s, lane length) (geometry.py:30-52: the
+ * segment by bisect_right on the cumulative lengths), gathered and ordered
+ * on the device.  Arrays of capacity `cap`; *n = records written.  Any
+ * output pointer may be NULL. */
+int tsb_records(tsb_engine* e, int32_t cap, int32_t* vix, int32_t* lane, int32_t* road_pos, double* s,
+                double* v, double* angle_deg, int32_t* n);
+
 /* Control surface, between steps only (world.py:716-740). */
 int tsb_set_lane(tsb_engine* e, int32_t lane, double max_speed, int32_t open);
 int tsb_set_signal_phase(tsb_engine* e, int32_t junction, int32_t phase);
@@ -234,7 +268,10 @@ int tsb_marks_elapsed(tsb_engine* e, int32_t a, int32_t b, double* ms);
  * resolver instead of the per-event fast path, bit 3 a step graph without
  * conditional nodes (every section's kernels launched, gating themselves),
  * bit 4 the parallel branches at default (not highest) priority, bit 5
- * one graph replay per step (no multi-step batch graph).
+ * one graph replay per step (no multi-step batch graph), bit 6 the
+ * snapshot-isolation check: before each update the step's write-before-read
+ * buffers (post-update records, sort scratch, the next layout) are filled
+ * with 0xff bytes (NaN / -1), so any read outside the snapshot shows.
  * Results must not change. */
 int tsb_set_debug(tsb_engine* e, int32_t flags);
 /* Which step paths ran so far (measurement hook): out[0] steps whose revert

@@ -33,6 +33,14 @@ SIGNATURES = {
     "tsb_finished": (_i32, [_vp, _i64, _i64, _vp, _vp, C.POINTER(_i64)]),
     "tsb_road_acc": (_i32, [_vp, _i32, _vp, _vp]),
     "tsb_min_front_gap": (_i32, [_vp, C.POINTER(_f64)]),
+    "tsb_get_vehicles": (_i32, [_vp, _vp, _i32, _vp]),
+    "tsb_grid_build": (_i32, [_i32, _i32, _f64, _i32, _f64, _i32, C.POINTER(_vp)]),
+    "tsb_grid_sizes": (_i32, [_vp, _vp]),
+    "tsb_grid_export": (_i32, [_vp, _vp]),
+    "tsb_grid_destroy": (None, [_vp]),
+    "tsb_py_dist": (_f64, [_f64, _f64, _f64, _f64]),
+    "tsb_set_geometry": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "tsb_records": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i32)]),
     "tsb_set_lane": (_i32, [_vp, _i32, _f64, _i32]),
     "tsb_set_signal_phase": (_i32, [_vp, _i32, _i32]),
     "tsb_signal_state": (_i32, [_vp, _vp, _vp]),

@@ -62,6 +62,16 @@ class TsbReport(C.Structure):
                                  "resolve_sequential", "reverts_total")]
 
 
+class TsbVehicleView(C.Structure):
+    _fields_ = [("s", C.c_double), ("v", C.c_double), ("finish_time", C.c_double),
+                ("lane", C.c_int32), ("road_pos", C.c_int32), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+# numpy view of an array of tsb_vehicle_view
+VIEW_DTYPE = np.dtype([("s", "<f8"), ("v", "<f8"), ("finish_time", "<f8"), ("lane", "<i4"),
+                       ("road_pos", "<i4"), ("status", "<i4"), ("pad", "<i4")])
+
+
 class TsbShard(C.Structure):
     _fields_ = [
         ("rank", C.c_int32), ("nranks", C.c_int32),

@@ -109,6 +109,14 @@ struct tsb_engine {
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
   int32_t launches_per_step = 0;
+  // queries (tsb_get_vehicles, tsb_records)
+  int32_t* q_loc = nullptr;
+  int32_t* q_bcnt = nullptr;
+  int32_t* q_i32 = nullptr;
+  double* q_f64 = nullptr;
+  int64_t* geo_off = nullptr;
+  double* geo_cum = nullptr;
+  double* geo_angle = nullptr;
   // profiling
   bool profiling = false;
   int n_ev = 0;
@@ -279,14 +287,22 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     {
       cudaStream_t main_s = e->cur;
       e->cur = e->side;
-      LAUNCH(KC_SPEEDS, k_speeds, grid_for(std::max(e->n_roads, 1), 128, 1 << 30), 128, c, 0);
+      LAUNCH(KC_SPEEDS, k_speeds, grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, 1 << 30), 256, c, 0);
       e->cur = main_s;
     }
     cudaEventRecord(e->ev_join, e->side);
+    if (c.debug & 64) LAUNCH(KC_MISC, k_poison, 148 * 8, 256, c);
+#if UPD_COMPACT
+    if (c.p.pow_glibc)
+      LAUNCH(KC_UPDATE, k_update_c<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+    else
+      LAUNCH(KC_UPDATE, k_update_c<false>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+#else
     if (c.p.pow_glibc)
       LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
     else
       LAUNCH(KC_UPDATE, k_update<false>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
+#endif
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
@@ -380,7 +396,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
 // Accumulates the current snapshot's road aggregate if the next step has not
 // done it yet (k_speeds); called before the aggregate is read.
 static int flush_speeds(tsb_engine* e) {
-  k_speeds<<<grid_for(std::max(e->n_roads, 1), 128, 1 << 30), 128, 0, e->stream>>>(e->c, 1);
+  k_speeds<<<grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, 1 << 30), 256, 0, e->stream>>>(e->c, 1);
   k_speeds_done<<<1, 1, 0, e->stream>>>(e->c);
   CK(cudaGetLastError());
   return TSB_OK;
@@ -1388,6 +1404,98 @@ int tsb_road_acc(tsb_engine* e, int32_t n_windows, double* sum, int64_t* count) 
       sum[(size_t)r * n_windows + w] = in ? s[(size_t)r * W + w] : 0.0;
       count[(size_t)r * n_windows + w] = in ? c[(size_t)r * W + w] : 0;
     }
+  return TSB_OK;
+}
+
+// ----------------------------------------------------------------- queries
+
+static int ensure_query_bufs(tsb_engine* e) {
+  if (e->q_loc) return TSB_OK;
+  const int64_t n = std::max<int32_t>(e->n_trips, 1);
+  const int64_t nb = (n + RECB - 1) / RECB;
+  RC(dalloc(e, &e->q_loc, n));
+  RC(dalloc(e, &e->q_bcnt, nb + 1));
+  RC(dalloc(e, &e->q_i32, 3 * n));
+  RC(dalloc(e, &e->q_f64, 3 * n));
+  return TSB_OK;
+}
+
+// vix -> snapshot record of every located vehicle (-1 elsewhere)
+static int locate(tsb_engine* e) {
+  RC(ensure_query_bufs(e));
+  CK(cudaMemsetAsync(e->q_loc, 0xff, sizeof(int32_t) * std::max<int32_t>(e->n_trips, 1), e->stream));
+  k_locate<<<grid_for(e->cap, 256, 148 * 16), 256, 0, e->stream>>>(e->c, e->q_loc);
+  CK(cudaGetLastError());
+  return TSB_OK;
+}
+
+int tsb_get_vehicles(tsb_engine* e, const int32_t* vix, int32_t n, tsb_vehicle_view* out) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  if (n < 0) return fail(TSB_EINVAL, "negative query size");
+  if (n == 0) return TSB_OK;
+  for (int32_t k = 0; k < n; k++)
+    if (vix[k] < 0 || vix[k] >= e->n_trips) return fail(TSB_ERANGE, "vehicle index %d out of range", vix[k]);
+  CK(cudaSetDevice(e->device));
+  RC(locate(e));
+  int32_t* dq = nullptr;
+  tsb_vehicle_view* dout = nullptr;
+  CK(cudaMallocAsync((void**)&dq, sizeof(int32_t) * n, e->stream));
+  CK(cudaMallocAsync((void**)&dout, sizeof(tsb_vehicle_view) * n, e->stream));
+  cudaError_t er = cudaMemcpyAsync(dq, vix, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e->stream);
+  if (er == cudaSuccess) {
+    k_vehicle_views<<<grid_for(n, 128, 148 * 8), 128, 0, e->stream>>>(e->c, e->q_loc, dq, n, dout);
+    er = cudaGetLastError();
+  }
+  if (er == cudaSuccess)
+    er = cudaMemcpyAsync(out, dout, sizeof(tsb_vehicle_view) * n, cudaMemcpyDeviceToHost, e->stream);
+  cudaFreeAsync(dq, e->stream);
+  cudaFreeAsync(dout, e->stream);
+  if (er == cudaSuccess) er = cudaStreamSynchronize(e->stream);
+  if (er != cudaSuccess) return fail(TSB_ECUDA, "tsb_get_vehicles: %s", cudaGetErrorString(er));
+  return TSB_OK;
+}
+
+int tsb_set_geometry(tsb_engine* e, const int64_t* geo_off, int64_t n_segments, const double* geo_cum,
+                     const double* geo_angle) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  if (n_segments < 0 || geo_off[0] != 0 || geo_off[e->n_lanes] != n_segments)
+    return fail(TSB_EINVAL, "geometry offsets do not cover the segments");
+  for (int32_t l = 0; l < e->n_lanes; l++)
+    if (geo_off[l + 1] < geo_off[l]) return fail(TSB_EINVAL, "geometry offsets not ascending");
+  CK(cudaSetDevice(e->device));
+  if (e->geo_off) return fail(TSB_EINVAL, "geometry already set");
+  RC(upload(e, &e->geo_off, geo_off, (size_t)e->n_lanes + 1));
+  RC(upload(e, &e->geo_cum, geo_cum, (size_t)n_segments));
+  RC(upload(e, &e->geo_angle, geo_angle, (size_t)n_segments));
+  return TSB_OK;
+}
+
+int tsb_records(tsb_engine* e, int32_t cap, int32_t* vix, int32_t* lane, int32_t* road_pos, double* s, double* v,
+                double* angle_deg, int32_t* n) {
+  if (!e) return fail(TSB_EINVAL, "null engine");
+  if (!e->geo_off) return fail(TSB_EINVAL, "tsb_records needs tsb_set_geometry first");
+  CK(cudaSetDevice(e->device));
+  *n = 0;
+  if (e->n_trips == 0) return TSB_OK;
+  RC(locate(e));
+  const int32_t nb = (e->n_trips + RECB - 1) / RECB;
+  k_rec_count<<<nb, RECB, 0, e->stream>>>(e->c, e->q_loc, e->q_bcnt);
+  k_rec_offsets<<<1, 1024, 0, e->stream>>>(e->q_bcnt, nb);
+  const int64_t N = e->n_trips;
+  RecOut o{e->q_i32, e->q_i32 + N, e->q_i32 + 2 * N, e->q_f64, e->q_f64 + N, e->q_f64 + 2 * N};
+  k_rec_write<<<nb, RECB, 0, e->stream>>>(e->c, e->q_loc, e->q_bcnt, o, e->geo_off, e->geo_cum, e->geo_angle);
+  CK(cudaGetLastError());
+  int32_t m = 0;
+  CK(cudaMemcpyAsync(&m, e->q_bcnt + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (m > cap) return fail(TSB_ECAP, "tsb_records: %d records, capacity %d", m, cap);
+  const void* src[6] = {o.vix, o.lane, o.road_pos, o.s, o.v, o.angle};
+  void* dst[6] = {vix, lane, road_pos, s, v, angle_deg};
+  const size_t sz[6] = {4, 4, 4, 8, 8, 8};
+  for (int k = 0; k < 6; k++)
+    if (dst[k] && m) CK(cudaMemcpyAsync(dst[k], src[k], sz[k] * m, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  *n = m;
   return TSB_OK;
 }
 

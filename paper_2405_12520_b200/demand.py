@@ -67,12 +67,17 @@ def preplaced_trips(net, router, n_vehicles: int, spacing: float, seed: int = 12
     no routable candidate are skipped.  The first ``n_vehicles`` are kept.
     """
     rng = random.Random(seed)
-    lanes = sorted(net.road_lane_ids())
+    if hasattr(net, "lane_kind"):  # a FlatNet (gridgen.grid_flat): same lanes, same lengths
+        lanes = [int(x) for x in np.nonzero(net.lane_kind == 0)[0]]
+        lane_len = net.lane_len.tolist()
+    else:
+        lanes = sorted(net.road_lane_ids())
+        lane_len = {lid: net.lanes[lid].length for lid in lanes}
     pool = sorted(rng.sample(lanes, min(pool_size, len(lanes))))
     reach = router.reachable_sets(pool)     # dest -> set-like of origins
     slots = []
     for lid in lanes:
-        length = net.lanes[lid].length
+        length = lane_len[lid]
         k = 0
         while spacing * k <= length:
             slots.append((lid, spacing * k))

@@ -38,6 +38,8 @@ class Router:
         self._h = h
 
     def _refresh(self, flat):
+        if self.net is None:  # built from a FlatNet alone (gridgen.grid_flat): flat is authoritative
+            return flat
         for lid, lane in self.net.lanes.items():
             flat.lane_cap[lid] = lane.max_speed
             flat.lane_open[lid] = 1 if lane.restriction == OPEN else 0

@@ -34,7 +34,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native, shard
-from .cabi import TsbReport, pack_network, pack_params, pack_shard, pack_trips
+from .cabi import VIEW_DTYPE, TsbReport, pack_network, pack_params, pack_shard, pack_trips
 from .errors import InputError
 from .flat import FlatNet, FlatTrips, flatten_network, flatten_trips
 from .params import EngineConfig
@@ -94,7 +94,19 @@ class ShardedWorld:
         _native.check(_native.lib().tsb_create_sharded(C.byref(pn.struct), C.byref(pt.struct), C.byref(params),
                                                        device, C.byref(ps.struct), C.byref(h)))
         self._h = h
+        geo_off = np.ascontiguousarray(flat.geo_off, dtype=np.int64)
+        geo_cum = np.ascontiguousarray(flat.geo_cum if len(flat.geo_cum) else np.zeros(1), dtype=np.float64)
+        geo_ang = np.ascontiguousarray(flat.geo_angle if len(flat.geo_angle) else np.zeros(1), dtype=np.float64)
+        _native.check(_native.lib().tsb_set_geometry(h, geo_off.ctypes.data, int(geo_off[-1]),
+                                                     geo_cum.ctypes.data, geo_ang.ctypes.data))
         self._report = TsbReport()
+        self.net = None
+        self._flat = flat
+        self._ft = ft
+        self._road_index = {rid: k for k, rid in enumerate(flat.road_ids)}
+        self._vix_of = {tid: k for k, tid in enumerate(ft.ids)}
+        self._finished: list = []
+        self._fin_seen = 0
         self.device = torch.device("cuda", device)
         # a packet holds at most every vehicle (32 B) plus one int32 count per lane entry
         n_exp = sum(len(x) for x in self.plan.export_lanes)
@@ -248,3 +260,120 @@ class ShardedWorld:
         m = nd.value
         own = (self.plan.zone[out["lane"][:m]] & shard.ZONE_OWN) > 0
         return {k: a[:m][own] for k, a in out.items()}
+
+    # ------------------------------------------------------------ queries (collective: every rank calls)
+    #
+    # The reference's query surface (world.py:706-714, 746-804, 771-782, 447-493)
+    # over the whole sharded network: each rank answers for its own lanes on the
+    # device (tsb_get_vehicles / tsb_records / tsb_finished / tsb_road_acc) and
+    # the answers are merged across ranks.
+
+    @property
+    def time(self) -> float:
+        return self._report.time
+
+    def _gather(self, obj) -> list:
+        out = [None] * self.nranks
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def get_vehicle(self, vehicle_id: int):
+        """StatusView of one vehicle: the rank driving it on its own lanes (or
+        where it finished / was dropped) answers; nobody -> still waiting."""
+        from .world import _STATUS, StatusView, _route_index
+
+        k = self._vix_of.get(vehicle_id)
+        if k is None:
+            raise InputError(f"unknown vehicle {vehicle_id}")
+        q = np.array([k], dtype=np.int32)
+        o = np.zeros(1, dtype=VIEW_DTYPE)
+        _native.check(_native.lib().tsb_get_vehicles(self._h, q.ctypes.data, 1, o.ctypes.data))
+        views = self._gather(o[0].tolist())
+        pick = next((v for v in views if v[5] in (1, 2, 3)), views[0])  # driving, finished, dropped
+        s, v, fin, lane, rp, st, _ = pick
+        status = _STATUS[st] if st >= 0 else _STATUS[0]
+        dep = float(self.ft.departure[k])
+        if status in ("driving", "finished"):
+            return StatusView(id=vehicle_id, lane_id=lane, s=s, v=v, status=status,
+                              route_index=_route_index(self.flat, lane, rp), depart_time=dep,
+                              finish_time=fin if status == "finished" else None)
+        return StatusView(id=vehicle_id, lane_id=int(self.ft.origin_lane[k]), s=float(self.ft.origin_s[k]),
+                          v=0.0, status=status, route_index=0, depart_time=dep, finish_time=None)
+
+    def records_arrays(self) -> dict:
+        """record_step's records over all ranks, sorted by id (each rank's own
+        lanes gathered and headed on its device, merged by vix)."""
+        n = max(len(self.ft.ids), 1)
+        bufs = {k: np.zeros(n, dtype=t) for k, t in (("vix", np.int32), ("lane", np.int32), ("road_pos", np.int32),
+                                                     ("s", np.float64), ("v", np.float64),
+                                                     ("angle_deg", np.float64))}
+        m = C.c_int32()
+        _native.check(_native.lib().tsb_records(self._h, n, *(bufs[k].ctypes.data for k in
+                                                            ("vix", "lane", "road_pos", "s", "v", "angle_deg")),
+                                                C.byref(m)))
+        parts = self._gather({k: a[:m.value] for k, a in bufs.items()})
+        out = {k: np.concatenate([p[k] for p in parts]) for k in bufs}
+        order = np.argsort(out["vix"], kind="stable")
+        out = {k: a[order] for k, a in out.items()}
+        ids = self.ft.ids
+        dense = len(ids) == 0 or (ids[0] == 0 and ids[-1] == len(ids) - 1)
+        out["id"] = out["vix"].astype(np.int64) if dense else np.array([ids[i] for i in out["vix"].tolist()],
+                                                                       dtype=object)
+        out["t"] = self.time
+        return out
+
+    def record_step(self, recorder) -> None:
+        from .records import VehicleRecord
+
+        r = self.records_arrays()
+        ids = self.ft.ids
+        for i, l, a, b, g in zip(r["vix"].tolist(), r["lane"].tolist(), r["s"].tolist(), r["v"].tolist(),
+                                 r["angle_deg"].tolist()):
+            recorder.write(VehicleRecord(t=r["t"], id=ids[i], lane=l, s=a, v=b, angle_deg=g))
+
+    @property
+    def finished(self) -> list:
+        """Arrivals of every rank merged in the reference's order (step, then
+        id: world.py:447-493 commits in id order; finish time = step end)."""
+        cap = max(len(self.ft.ids), 1)
+        vix = np.zeros(cap, dtype=np.int32)
+        t = np.zeros(cap, dtype=np.float64)
+        n = C.c_int64()
+        _native.check(_native.lib().tsb_finished(self._h, self._fin_seen, cap, vix.ctypes.data, t.ctypes.data,
+                                                 C.byref(n)))
+        self._fin_seen += n.value
+        parts = self._gather((vix[:n.value], t[:n.value]))
+        new = sorted((float(tt), int(x)) for pv, pt in parts for x, tt in zip(pv.tolist(), pt.tolist()))
+        dep, ids = self.ft.departure, self.ft.ids
+        self._finished.extend((ids[x], float(dep[x]), tt) for tt, x in new)
+        return self._finished
+
+    def _road_acc(self):
+        """Road aggregate over ranks (each road accumulated by its owner only)."""
+        torch = self.torch
+        nw = int(self.time / self.config.speed_window) + 2
+        nr = len(self.flat.road_ids)
+        s = np.zeros((max(nr, 1), nw), dtype=np.float64)
+        c = np.zeros((max(nr, 1), nw), dtype=np.int64)
+        _native.check(_native.lib().tsb_road_acc(self._h, nw, s.ctypes.data, c.ctypes.data))
+        ts, tc = torch.from_numpy(s), torch.from_numpy(c)
+        if not self.host_staging:
+            ts, tc = ts.to(self.device), tc.to(self.device)
+        self.dist.all_reduce(ts, group=self.group)
+        self.dist.all_reduce(tc, group=self.group)
+        return ts.cpu().numpy()[:nr], tc.cpu().numpy()[:nr]
+
+    def road_free_flow(self, road_id: str) -> float:
+        from .world import World
+
+        return World.road_free_flow(self, road_id)
+
+    def get_road_speed(self, road_id: str, window: tuple[float, float]) -> float:
+        from .world import World
+
+        return World.get_road_speed(self, road_id, window)
+
+    def road_windows(self, horizon: float) -> list:
+        from .world import World
+
+        return World.road_windows(self, horizon)

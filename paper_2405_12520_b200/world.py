@@ -7,9 +7,11 @@ step, the vehicle state resident in HBM, and host round trips only for
 queries.  There is no CPU fallback: without the native library or a CUDA
 device, construction raises ``EngineError``.
 
-Queries download lazily: the first query after a step fetches the snapshot
-layout once (the per-lane index of world.py:227-242) and answers every
-``get_vehicle`` / ``prepare`` / ``record_step`` from that copy.
+Queries run on the device: ``get_vehicle`` gathers just the requested
+vehicle (tsb_get_vehicles), ``record_step`` / ``records_arrays`` receive the
+id-sorted records with their headings (tsb_records).  ``prepare`` -- the
+whole per-lane index of world.py:227-242 by definition -- downloads the
+snapshot layout once per step.
 """
 
 from __future__ import annotations
@@ -21,9 +23,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .cabi import TsbReport, pack_network, pack_params, pack_trips
+from .cabi import VIEW_DTYPE, TsbReport, pack_network, pack_params, pack_trips
 from .errors import InputError
-from .flat import KIND_CONNECTOR, FlatNet, FlatTrips, flatten_network, flatten_trips, record_angles
+from .flat import KIND_CONNECTOR, FlatNet, FlatTrips, flatten_network, flatten_trips
 from .network import CLOSED, OPEN
 from .params import EngineConfig
 from .records import RoadWindow, VehicleRecord
@@ -80,6 +82,17 @@ class SimulationOutput:
         return [fin - dep for _, dep, fin in self.finished]
 
 
+def _route_index(flat: FlatNet, lane: int, rp: int) -> int:
+    # route_index == 2 * road_pos + (lane is a connector): invariant of
+    # world.py:478-487 under transitions, lane changes and reverts
+    return 2 * rp + (1 if flat.lane_kind[lane] == KIND_CONNECTOR else 0)
+
+
+def _nonempty_f64(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if a.size else np.zeros(1, dtype=np.float64)
+
+
 class World:
     """B200 engine behind the reference ``World`` interface."""
 
@@ -103,6 +116,12 @@ class World:
         _native.check(_native.lib().tsb_create(C.byref(packed_net.struct), C.byref(packed_trips.struct),
                                                C.byref(params), device, C.byref(h)))
         self._h = h
+        f = self._flat
+        geo_off = np.ascontiguousarray(f.geo_off, dtype=np.int64)
+        geo_cum = _nonempty_f64(f.geo_cum)
+        geo_ang = _nonempty_f64(f.geo_angle)
+        _native.check(_native.lib().tsb_set_geometry(h, geo_off.ctypes.data, int(geo_off[-1]),
+                                                     geo_cum.ctypes.data, geo_ang.ctypes.data))
         self.router = Router(net, flat=self._flat) if net is not None else None
         self._report = TsbReport()
         self._finished: list[tuple[int, float, float]] = []
@@ -257,31 +276,30 @@ class World:
         return index, snapshot
 
     def _route_index(self, lane: int, rp: int) -> int:
-        # route_index == 2 * road_pos + (lane is a connector): invariant of
-        # world.py:478-487 under transitions, lane changes and reverts
-        return 2 * rp + (1 if self._flat.lane_kind[lane] == KIND_CONNECTOR else 0)
+        return _route_index(self._flat, lane, rp)
+
+    def vehicle_views(self, vix) -> np.ndarray:
+        """Device-side StatusView data for dense vehicle indices (tsb_get_vehicles):
+        a structured array (s, v, finish_time, lane, road_pos, status)."""
+        q = np.ascontiguousarray(vix, dtype=np.int32)
+        out = np.zeros(len(q), dtype=VIEW_DTYPE)
+        _native.check(_native.lib().tsb_get_vehicles(self._live(), q.ctypes.data, len(q), out.ctypes.data))
+        return out
+
+    def _status_view(self, vehicle_id: int, k: int, o) -> StatusView:
+        status = _STATUS[int(o["status"])]
+        lane, rp = int(o["lane"]), int(o["road_pos"])
+        return StatusView(id=vehicle_id, lane_id=lane, s=float(o["s"]), v=float(o["v"]), status=status,
+                          route_index=self._route_index(lane, rp) if status in (DRIVING, FINISHED) else 0,
+                          depart_time=float(self._ft.departure[k]),
+                          finish_time=float(o["finish_time"]) if status == FINISHED else None)
 
     def get_vehicle(self, vehicle_id: int) -> StatusView:
+        """world.py:706-714, answered on the device for this one vehicle."""
         k = self._vix_of.get(vehicle_id)
         if k is None:
             raise InputError(f"unknown vehicle {vehicle_id}")
-        m = self._state()
-        status = _STATUS[int(m["status"][k])]
-        dep = float(self._ft.departure[k])
-        if status == DRIVING:
-            p = int(m["pos"][k])
-            lane, rp = int(m["lane"][p]), int(m["rp"][p])
-            return StatusView(id=vehicle_id, lane_id=lane, s=float(m["s"][p]), v=float(m["v"][p]),
-                              status=status, route_index=self._route_index(lane, rp),
-                              depart_time=dep, finish_time=None)
-        if status == FINISHED:
-            lane, rp = int(m["l_lane"][k]), int(m["l_rp"][k])
-            return StatusView(id=vehicle_id, lane_id=lane, s=float(m["l_s"][k]), v=float(m["l_v"][k]),
-                              status=status, route_index=self._route_index(lane, rp),
-                              depart_time=dep, finish_time=float(m["finish"][k]))
-        return StatusView(id=vehicle_id, lane_id=int(self._ft.origin_lane[k]),
-                          s=float(self._ft.origin_s[k]), v=0.0, status=status, route_index=0,
-                          depart_time=dep, finish_time=None)
+        return self._status_view(vehicle_id, k, self.vehicle_views([k])[0])
 
     def min_front_gap(self) -> float:
         g = C.c_double()
@@ -292,17 +310,27 @@ class World:
 
     def records_arrays(self) -> dict:
         """The step's vehicle records as numpy arrays, sorted by id -- the batch
-        form of record_step (world.py:771-782): keys
-        ``t`` (float), ``vix`` (dense index), ``id``, ``lane``, ``s``, ``v``,
-        ``angle_deg`` (geometry.py:45-52)."""
-        m = self._state()
-        order = np.argsort(m["vix"], kind="stable")
-        vix, lane, s, v = m["vix"][order], m["lane"][order], m["s"][order], m["v"][order]
+        form of record_step (world.py:771-782), gathered,
+        id-ordered and given their headings (geometry.py:45-52) on the device
+        (tsb_records): keys ``t`` (float), ``vix`` (dense index), ``id``,
+        ``lane``, ``road_pos``, ``s``, ``v``, ``angle_deg``."""
+        n = max(self.total_trips, 1)
+        vix = np.zeros(n, dtype=np.int32)
+        lane = np.zeros(n, dtype=np.int32)
+        rp = np.zeros(n, dtype=np.int32)
+        s = np.zeros(n, dtype=np.float64)
+        v = np.zeros(n, dtype=np.float64)
+        ang = np.zeros(n, dtype=np.float64)
+        m = C.c_int32()
+        _native.check(_native.lib().tsb_records(self._live(), n, vix.ctypes.data, lane.ctypes.data, rp.ctypes.data,
+                                                s.ctypes.data, v.ctypes.data, ang.ctypes.data, C.byref(m)))
+        k = m.value
+        vix = vix[:k]
         ids = self._ft.ids
         dense = len(ids) == 0 or (ids[0] == 0 and ids[-1] == len(ids) - 1)
         id_arr = vix.astype(np.int64) if dense else np.array([ids[i] for i in vix.tolist()], dtype=object)
-        return {"t": self.time, "vix": vix, "id": id_arr, "lane": lane, "s": s, "v": v,
-                "angle_deg": record_angles(self._flat, lane, s)}
+        return {"t": self.time, "vix": vix, "id": id_arr, "lane": lane[:k], "road_pos": rp[:k], "s": s[:k],
+                "v": v[:k], "angle_deg": ang[:k]}
 
     def record_step(self, recorder) -> None:
         """One VehicleRecord per driving vehicle, sorted by id (world.py:771-782)."""

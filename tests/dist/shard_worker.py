@@ -78,6 +78,33 @@ def stall_test():
         print(f"STALL_RESULT ok={int(ok)} msg={msg!r}", flush=True)
 
 
+def check_queries(sw, ref, rank, k) -> int:
+    """The merged query surface of the sharded engine (collective) against the
+    single engine: id-sorted records with headings, arrivals in reference
+    order, road windows, and get_vehicle for a sample of ids."""
+    bad = 0
+    a, b = sw.records_arrays(), ref.records_arrays()
+    for key in ("vix", "lane", "road_pos", "s", "v", "angle_deg"):
+        if not np.array_equal(a[key], b[key]):
+            print(f"rank {rank} step {k}: records field {key} differs", flush=True)
+            bad += 1
+            break
+    if sw.finished != ref.finished:
+        print(f"rank {rank} step {k}: finished lists differ ({len(sw.finished)} vs {len(ref.finished)})", flush=True)
+        bad += 1
+    if sw.road_windows(ref.time) != ref.road_windows(ref.time):
+        print(f"rank {rank} step {k}: road windows differ", flush=True)
+        bad += 1
+    rng = np.random.default_rng(k)
+    ids = ref._ft.ids
+    for i in rng.choice(len(ids), min(25, len(ids)), replace=False).tolist():
+        if sw.get_vehicle(ids[i]) != ref.get_vehicle(ids[i]):
+            print(f"rank {rank} step {k}: get_vehicle({ids[i]}) differs", flush=True)
+            bad += 1
+            break
+    return bad
+
+
 def main():
     name, steps = sys.argv[1], int(sys.argv[2])
     p2p = len(sys.argv) > 3 and sys.argv[3] == "p2p"
@@ -112,6 +139,8 @@ def main():
                     print(f"rank {rank} step {k}: own-lane field {key} differs", flush=True)
                     bad += 1
                     break
+        if k % 50 == 0 or k == steps:
+            bad += check_queries(sw, ref, rank, k)
         if agree_bad(bad):
             break
     ex = sw.exchange_bytes()

@@ -93,6 +93,20 @@ def test_dense_short_blocks_revert_chains(debug):
     _close(g, r)
 
 
+@pytest.mark.parametrize("debug", [64, 64 | 2 | 8])
+def test_snapshot_isolation_poisoned_scratch(debug):
+    """Debug bit 6 fills every write-before-read buffer of the step (post-update
+    records, sort scratch, the layout the step builds) with 0xff bytes before
+    the update: results identical to the oracle means every kernel reads only
+    the snapshot and what the step itself wrote (world.py:231-236, 416-419).
+    With the full regroup (bit 1) and the gated graph (bit 3) as well."""
+    net = generate_grid(5, 5, block_length=80.0, lanes_per_direction=2)
+    trips = random_trips(net, 6000, seed=5, window=(0.0, 300.0))
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 5, 300, every=3, debug=debug)
+    assert reverts > 50
+    _close(g, r)
+
+
 def test_dense_two_lane_reverts():
     net = generate_grid(5, 5, block_length=80.0, lanes_per_direction=2)
     trips = random_trips(net, 6000, seed=5, window=(0.0, 300.0))
