@@ -731,48 +731,100 @@ static int cmp_lane_then_s(const void* a, const void* b) {
   return x < y ? -1 : 1;
 }
 
-/* world.py:509-559, including the restart after every revert */
+/* world.py:509-559, including the restart after every revert.
+ *
+ * Statement for statement the reference's loop: every pass regroups the
+ * driving vehicles by lane (world.py:520-522: lanes in id order, members
+ * sorted by (-s, id)) and sweeps the lanes in order until the first revert,
+ * then starts over from the first lane.  Two bookkeeping shortcuts keep a
+ * pass from costing a full sort of the driving set (C4-size parity cases)
+ * without changing what any sweep computes:
+ *  - the groups are updated incrementally (a pass's groups equal the
+ *    previous pass's except for the lanes a revert moved a vehicle between;
+ *    a lane whose members' s changed is re-sorted before its next sweep);
+ *  - a lane whose last sweep changed nothing, and whose members have not
+ *    changed since, is skipped: its sweep is a deterministic function of
+ *    exactly that unchanged state, so re-running it would again change
+ *    nothing (the reference re-runs it). */
+static int cmp_lane_member(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  const veh_t *p = &g_cur->V[x], *q = &g_cur->V[y];
+  if (p->s != q->s) return p->s > q->s ? -1 : 1;
+  return x < y ? -1 : 1;
+}
+
+static int same_bits(double a, double b) { return memcmp(&a, &b, sizeof(double)) == 0; }
+
 static void collision_sweep(orc* o) {
   double floor_gap = o->p.s0_floor, dt = o->p.dt, L = o->p.vehicle_length;
+  const int32_t nl = o->nl;
   int32_t* grp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(o->n_driving + 1));
+  ivec* lanes = (ivec*)calloc((size_t)nl, sizeof(ivec));
+  uint8_t* resort = (uint8_t*)calloc((size_t)nl, 1);
+  uint8_t* clean = (uint8_t*)calloc((size_t)nl, 1);
+  int32_t n = sorted_driving(o, grp);
+  for (int32_t k = 0; k < n; k++) iv_push(&lanes[o->V[grp[k]].lane], grp[k]);
+  g_cur = o;
+  for (int32_t l = 0; l < nl; l++)
+    if (lanes[l].n > 1) qsort(lanes[l].v, (size_t)lanes[l].n, sizeof(int32_t), cmp_lane_member);
   o->reverts_last = 0;
   for (int32_t pass = 0; pass < o->n_driving + 2; pass++) {
-    int32_t n = sorted_driving(o, grp);
-    g_cur = o;
-    qsort(grp, (size_t)n, sizeof(int32_t), cmp_lane_then_s);
     int dirty = 0;
-    int32_t i = 0;
-    while (i < n && !dirty) {
-      int32_t lane = o->V[grp[i]].lane, j = i;
-      while (j < n && o->V[grp[j]].lane == lane) j++;
+    for (int32_t lane = 0; lane < nl && !dirty; lane++) {
+      ivec* g = &lanes[lane];
+      if (g->n == 0 || clean[lane]) continue;
+      if (resort[lane]) {
+        g_cur = o;
+        if (g->n > 1) qsort(g->v, (size_t)g->n, sizeof(int32_t), cmp_lane_member);
+        resort[lane] = 0;
+      }
+      int changed = 0;
       veh_t* prev = NULL;
+      int32_t prev_k = -1;
       double prev_rear = INFINITY;
-      for (int32_t k = i; k < j; k++) {
-        veh_t* vh = &o->V[grp[k]];
+      for (int32_t k = 0; k < g->n; k++) {
+        veh_t* vh = &o->V[g->v[k]];
         double limit = prev_rear - floor_gap;
         if (vh->s > limit + 1e-12) {
           int entered = vh->lane != vh->snap_lane;
           double floor_s = entered ? 0.0 : vh->snap_s;
+          int32_t moved = -1;  /* member index reverted out of this lane */
+          const double s_was = vh->s, v_was = vh->v;
           if (limit >= floor_s) {
             vh->v = py_max(0.0, py_min(vh->v, vh->v - (vh->s - limit) / dt));
             vh->s = limit;
           } else if (entered && !vh->reverted) {
             revert(vh);
-            dirty = 1;
-            break;
+            moved = k;
           } else if (prev && prev->lane != prev->snap_lane && !prev->reverted) {
             revert(prev);
-            dirty = 1;
-            break;
+            moved = prev_k;
           } else {
             vh->v = 0.0;
             vh->s = floor_s;
           }
+          if (moved >= 0) {
+            const int32_t vx = g->v[moved];
+            for (int32_t q = moved; q + 1 < g->n; q++) g->v[q] = g->v[q + 1];
+            g->n--;
+            const int32_t to = o->V[vx].lane;
+            iv_push(&lanes[to], vx);
+            resort[to] = 1;
+            clean[to] = 0;
+            clean[lane] = 0;
+            dirty = 1;
+            break;
+          }
+          if (!same_bits(s_was, vh->s) || !same_bits(v_was, vh->v)) {
+            changed = 1;
+            resort[lane] = 1;
+          }
         }
         prev = vh;
+        prev_k = k;
         prev_rear = vh->s - L;
       }
-      i = j;
+      if (!dirty) clean[lane] = changed ? 0 : 1;
     }
     if (dirty) {
       o->reverts_last++;
@@ -780,6 +832,10 @@ static void collision_sweep(orc* o) {
     }
     if (!dirty) break;
   }
+  for (int32_t l = 0; l < nl; l++) free(lanes[l].v);
+  free(lanes);
+  free(resort);
+  free(clean);
   free(grp);
 }
 

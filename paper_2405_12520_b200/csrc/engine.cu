@@ -114,6 +114,10 @@ struct tsb_engine {
   int32_t* q_bcnt = nullptr;
   int32_t* q_i32 = nullptr;
   double* q_f64 = nullptr;
+  bool loc_valid = false;  // q_loc describes the current snapshot
+  int64_t q_cap = 0;       // tsb_get_vehicles query capacity
+  uint8_t* q_dev = nullptr;
+  uint8_t* q_host = nullptr;
   int64_t* geo_off = nullptr;
   double* geo_cum = nullptr;
   double* geo_angle = nullptr;
@@ -292,17 +296,10 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     }
     cudaEventRecord(e->ev_join, e->side);
     if (c.debug & 64) LAUNCH(KC_MISC, k_poison, 148 * 8, 256, c);
-#if UPD_COMPACT
-    if (c.p.pow_glibc)
-      LAUNCH(KC_UPDATE, k_update_c<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
-    else
-      LAUNCH(KC_UPDATE, k_update_c<false>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
-#else
     if (c.p.pow_glibc)
       LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
     else
       LAUNCH(KC_UPDATE, k_update<false>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
-#endif
   }
   if (phase == 1) return;
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
@@ -705,6 +702,7 @@ static int build_graph(tsb_engine* e) {
 }
 
 static int do_steps(tsb_engine* e, int32_t n) {
+  e->loc_valid = false;
   if (n <= 0) return TSB_OK;
   RC(ensure_windows(e, n));
   if (e->routes_stale) {
@@ -1144,6 +1142,7 @@ int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes) {
 }
 
 int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes) {
+  if (e) e->loc_valid = false;
   if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
   Ctx& c = e->c;
   SrcBase sb{};
@@ -1243,6 +1242,7 @@ int tsb_set_p2p_timeout(tsb_engine* e, double seconds) {
 }
 
 int tsb_shard_p2p_exchange(tsb_engine* e) {
+  if (e) e->loc_valid = false;
   if (!e || !e->c.sharded || !e->p2p_ready) return fail(TSB_EINVAL, "P2P exchange not set up");
   Launcher L{e};
   issue_exchange(e, L);
@@ -1260,6 +1260,8 @@ void tsb_destroy(tsb_engine* e) {
   for (int q = 0; q < 2 * 96; q++)
     if (e->ev[q]) cudaEventDestroy(e->ev[q]);
   for (void* p : e->allocs) cudaFree(p);
+  if (e->q_dev) cudaFree(e->q_dev);
+  if (e->q_host) cudaFreeHost(e->q_host);
   if (e->dyn_host) cudaFreeHost(e->dyn_host);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->body) cudaStreamDestroy(e->body);
@@ -1420,12 +1422,15 @@ static int ensure_query_bufs(tsb_engine* e) {
   return TSB_OK;
 }
 
-// vix -> snapshot record of every located vehicle (-1 elsewhere)
+// vix -> snapshot record of every located vehicle (-1 elsewhere); computed
+// once per snapshot (every step and ghost import invalidates it)
 static int locate(tsb_engine* e) {
   RC(ensure_query_bufs(e));
+  if (e->loc_valid) return TSB_OK;
   CK(cudaMemsetAsync(e->q_loc, 0xff, sizeof(int32_t) * std::max<int32_t>(e->n_trips, 1), e->stream));
   k_locate<<<grid_for(e->cap, 256, 148 * 16), 256, 0, e->stream>>>(e->c, e->q_loc);
   CK(cudaGetLastError());
+  e->loc_valid = true;
   return TSB_OK;
 }
 
@@ -1437,21 +1442,29 @@ int tsb_get_vehicles(tsb_engine* e, const int32_t* vix, int32_t n, tsb_vehicle_v
     if (vix[k] < 0 || vix[k] >= e->n_trips) return fail(TSB_ERANGE, "vehicle index %d out of range", vix[k]);
   CK(cudaSetDevice(e->device));
   RC(locate(e));
-  int32_t* dq = nullptr;
-  tsb_vehicle_view* dout = nullptr;
-  CK(cudaMallocAsync((void**)&dq, sizeof(int32_t) * n, e->stream));
-  CK(cudaMallocAsync((void**)&dout, sizeof(tsb_vehicle_view) * n, e->stream));
-  cudaError_t er = cudaMemcpyAsync(dq, vix, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e->stream);
-  if (er == cudaSuccess) {
-    k_vehicle_views<<<grid_for(n, 128, 148 * 8), 128, 0, e->stream>>>(e->c, e->q_loc, dq, n, dout);
-    er = cudaGetLastError();
+  // query and answer buffers: persistent, grown on demand (pinned host staging)
+  if (n > e->q_cap) {
+    if (e->q_dev) cudaFree(e->q_dev);
+    if (e->q_host) cudaFreeHost(e->q_host);
+    e->q_dev = nullptr;
+    e->q_host = nullptr;
+    const int64_t cap = std::max<int64_t>(n, 1024);
+    const size_t bytes = (size_t)cap * (sizeof(int32_t) + sizeof(tsb_vehicle_view));
+    CK(cudaMalloc((void**)&e->q_dev, bytes));
+    CK(cudaMallocHost((void**)&e->q_host, bytes));
+    e->q_cap = cap;
   }
-  if (er == cudaSuccess)
-    er = cudaMemcpyAsync(out, dout, sizeof(tsb_vehicle_view) * n, cudaMemcpyDeviceToHost, e->stream);
-  cudaFreeAsync(dq, e->stream);
-  cudaFreeAsync(dout, e->stream);
-  if (er == cudaSuccess) er = cudaStreamSynchronize(e->stream);
-  if (er != cudaSuccess) return fail(TSB_ECUDA, "tsb_get_vehicles: %s", cudaGetErrorString(er));
+  int32_t* hq = (int32_t*)e->q_host;
+  tsb_vehicle_view* hv = (tsb_vehicle_view*)(e->q_host + (size_t)e->q_cap * sizeof(int32_t));
+  int32_t* dq = (int32_t*)e->q_dev;
+  tsb_vehicle_view* dv = (tsb_vehicle_view*)(e->q_dev + (size_t)e->q_cap * sizeof(int32_t));
+  std::memcpy(hq, vix, sizeof(int32_t) * n);
+  CK(cudaMemcpyAsync(dq, hq, sizeof(int32_t) * n, cudaMemcpyHostToDevice, e->stream));
+  k_vehicle_views<<<grid_for(n, 128, 148 * 8), 128, 0, e->stream>>>(e->c, e->q_loc, dq, n, dv);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hv, dv, sizeof(tsb_vehicle_view) * n, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  std::memcpy(out, hv, sizeof(tsb_vehicle_view) * n);
   return TSB_OK;
 }
 

@@ -253,9 +253,6 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #ifndef UPD_GRID_CAP
 #define UPD_GRID_CAP (1 << 30)
 #endif
-#ifndef UPD_COMPACT
-#define UPD_COMPACT 1  // k_update_c (MOBIL sides compacted across the block) instead of k_update
-#endif
 #ifndef MOBIL_UNROLL
 #define MOBIL_UNROLL 2
 #endif
@@ -464,448 +461,6 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     } else {
       found = true;
     }
-    if (!found) {
-      const double remaining = L1.len - s;
-      bool stop = false;
-      if (L1.kind == TSB_KIND_ROAD) {
-        if (next_road < 0) {
-          gap = CUDART_INF;
-          lead_v = 0.0;
-          found = true;
-        } else {
-          const int32_t conn = conn_from_id(c, lane, next_road);
-          const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
-          if (conn < 0 || !lf_passable(f)) {
-            stop = true;
-          } else {
-            const int asp = lf_aspect(f);
-            if (asp == RED || (asp == AMBER && remaining > v * v / (2.0 * p.b))) stop = true;
-          }
-        }
-        if (stop) {
-          gap = py_max(remaining, EPS_GAP);
-          lead_v = 0.0;
-          found = true;
-        }
-      }
-      if (!found) {
-        const int32_t* rq = roads;
-        LaneRec LC = L1;
-        int32_t cur = lane;
-        double dist = remaining;
-        gap = CUDART_INF;
-        lead_v = 0.0;
-        while (dist < p.lookahead) {
-          int32_t nxt;
-          if (LC.kind == TSB_KIND_ROAD) {
-            const int32_t nr = rq == roads ? next_road : __ldg(rq + 1);
-            nxt = nr < 0 ? -1 : conn_from_id(c, cur, nr);
-            if (nxt < 0 || !(c.lflag[nxt] & LF_OPEN)) break;
-          } else {
-            nxt = LC.succ1;
-            rq += 1;
-            if (!(c.lflag[nxt] & LF_OPEN)) break;
-          }
-          const int2 sgx = seg(c, S, nxt);
-          const int32_t lo = sgx.x, hi = sgx.y;
-          if (hi > lo) {
-            const VRec rear = A[hi - 1];
-            double g = dist + rear.s - Lv;
-            gap = py_max(g, EPS_GAP);
-            lead_v = rear.v;
-            break;
-          }
-          LC = c.lanes[nxt];
-          cur = nxt;
-          dist += LC.len;
-        }
-      }
-    }
-
-    // ---- IDM + integration (world.py:406-419)
-    double a;
-    if (have_final) {
-      a = a_final;
-    } else {
-      const double v0e = py_min(p.v0, L1.cap);
-      const double fr = (have_fr_me && v0e == v0e_cur) ? fr_me : idm_free<G>(p, v, v0e);
-      a = idm_with_free<G>(p, fr, v, v - lead_v, gap);
-    }
-    const double dt = p.dt;
-    double v_new = v + a * dt, disp;
-    if (v_new <= 0.0) {
-      v_new = 0.0;
-      disp = a < 0.0 ? div_pos(v * v, 2.0 * -a) : 0.0;
-    } else {
-      disp = v * dt + 0.5 * a * dt * dt;
-      if (disp < 0.0) disp = 0.0;
-    }
-    double ns = s + disp, nv = v_new;
-    int32_t nl = lane, nptr = me.rptr, nxt_rd = next_road;
-
-    // ---- _apply_deltas transitions (world.py:443-499)
-    LaneRec LT = L1;
-    bool arrived = false, host = false;
-    while (ns > LT.len) {
-      if (LT.kind == TSB_KIND_ROAD) {
-        const int32_t nr = nxt_rd;
-        if (nr < 0) {
-          arrived = true;
-          break;
-        }
-        const int32_t conn = conn_from_id(c, nl, nr);
-        const uint8_t f = conn >= 0 ? c.lflag[conn] : 0;
-        if (conn >= 0 && !lf_passable(f)) {
-          host = true;  // reroute needs the host router (world.py:460-469)
-          break;
-        }
-        if (conn < 0 || lf_aspect(f) == RED) {
-          ns = LT.len;
-          nv = 0.0;
-          break;
-        }
-        ns -= LT.len;
-        nl = conn;
-        LT = c.lanes[conn];
-      } else {
-        ns -= LT.len;
-        nl = LT.succ1;
-        nptr += 1;
-        nxt_rd = __ldg(c.routes + nptr + 1);
-        LT = c.lanes[nl];
-      }
-    }
-    VRec out{ns, nv, me.vix, nptr, nl, i};
-    nrc_cur[i] = make_int2(nptr, nxt_rd);
-    if (arrived && ghost) {  // the owner records it
-      out.lane = -1;
-      c.stay[i] = 0;
-    } else if (arrived) {
-      out.lane = -1;
-      c.stay[i] = 0;
-      c.status[me.vix] = TSB_STATUS_FINISHED;
-      c.finish[me.vix] = new_time;
-      c.fin_state[me.vix] = me;
-      unsigned long long k = atomicAdd((unsigned long long*)&dy->finished_now, 1ULL);
-      FinEntry fe;
-      fe.vix = me.vix;
-      fe.pad = 0;
-      fe.step = (int64_t)step_no;
-      c.fin_log[dy->fin_log_n + (int64_t)k] = fe;
-    } else if (host) {
-      int32_t k = atomicAdd(&dy->n_hostq, 1);
-      c.hostq[k] = i;
-      if (!c.split) {  // closures only occur in split mode; keep the state consistent
-        out.lane = nl;
-        count_bucket(c, nl, snap_lane, i);
-      }
-    } else {
-      count_bucket(c, nl, snap_lane, i);
-      if (ghost && (c.zone[nl] & ZF_OWN)) c.status[me.vix] = TSB_STATUS_DRIVING;  // entered an own lane
-    }
-    c.B[i] = out;
-  }
-}
-
-// ------------------------------------------------------------------ k_update (side-compacted)
-//
-// The same per-vehicle computation as k_update, with MOBIL's side
-// evaluations (mobil.evaluate_change per candidate lane, mobil.py:45-98)
-// compacted across the block: in phase 1 each thread (one snapshot record)
-// evaluates its RNG gate and the side-independent MOBIL terms, and lists the
-// sides that can still be chosen -- a lateral lane that exists, is open and
-// (discretionary change) connects to the next road of the route
-// (world.py:337-342, 366-372); every other side is discarded by the
-// reference before its result matters.  Phase 2 evaluates the listed sides
-// with every thread of the block (a warp no longer runs both sides for every
-// vehicle, nor idles on connector or single-lane vehicles); phase 3 picks the
-// best side per vehicle in the reference's order (larger incentive, tie ->
-// smaller lane id) and finishes the update.  Same fp64 expressions on the
-// same operands: results are bit-identical to k_update.
-// Per-thread context of phase 1, read by phase 2 (the thread's side tasks)
-// and phase 3 (the owner): registers stay free for phase 2's evaluations.
-struct __align__(8) UpdCtx {
-  double fr_me, a_me, v0e, d_of, len;
-  int32_t next_road, nb0, nb1, snap_lane;
-  uint32_t flags;  // UF_*
-  int32_t pad;
-};
-enum : uint32_t { UF_GO = 1, UF_PREV = 2, UF_FRME = 4, UF_FINC = 8, UF_MAND = 16 };
-struct __align__(8) MobRes {
-  double inc, s_t, a_new;
-  int32_t tl;
-  int32_t ok;  // bit 0 chosen-able, bit 1 target-leader gap >= 1e-6
-};
-
-template <bool G>
-__global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update_c(Ctx c) {
-  __shared__ UpdCtx mc[UPD_BT];
-  __shared__ MobRes mr[2][UPD_BT];
-  __shared__ uint16_t tasks[2 * UPD_BT];
-  __shared__ int32_t ntask;
-  PDL_WAIT();
-  TL_MARK(TL_UPDATE);
-  Dyn* dy = c.dyn;
-  const int32_t n_a = dy->n_a;
-  const int32_t n = n_a + (c.sharded ? dy->n_g : 0);
-  const VRec* A = c.lay[dy->cur];
-  const int2* S = c.rng[dy->cur];
-  const Params& p = c.p;
-  const uint64_t step_no = (uint64_t)dy->step_no;
-  const double new_time = dy->time + p.dt;
-  const double Lv = p.L;
-  const int2* nrc_prev = c.nrc[(step_no + 1) & 1];
-  int2* nrc_cur = c.nrc[step_no & 1];
-  const int tid = threadIdx.x;
-  for (int32_t base = blockIdx.x * UPD_BT; base < n; base += gridDim.x * UPD_BT) {
-    if (tid == 0) ntask = 0;
-    const int32_t i = base + tid;
-    // ---------------- phase 1: load, stale check, RNG gate, shared MOBIL terms
-    bool live = i < n;
-    VRec me = VRec{0.0, 0.0, 0, 0, -1, 0};
-    int32_t snap_lane = -1;
-    bool ghost = false, has_prev = false, has_next = false;
-    VRec prv = VRec{0.0, 0.0, 0, 0, -1, 0};
-    LaneRec L0;
-    int32_t next_road = -1;
-    double v = 0.0, v0e_cur = 0.0, fr_me = 0.0, a_me = 0.0, g_cur = 0.0;
-    bool have_fr_me = false, go = false, mobil = false, mandatory = false;
-    int32_t sides0 = -1, sides1 = -1;
-    unsigned my_tasks = 0;
-    if (live) {
-      me = A[i];
-      snap_lane = me.lane;
-      ghost = c.sharded && i >= n_a;
-      const VRec prv_ = A[i > 0 ? i - 1 : i];
-      const VRec nxv_ = A[i + 1 < n ? i + 1 : i];
-      const int2 sg0 = seg(c, S, snap_lane);
-      if (i < sg0.x || i >= sg0.y || (c.sharded && !ghost && !(c.zone[snap_lane] & ZF_OWN))) {
-        c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
-        c.stay[i] = 0;
-        live = false;
-      } else {
-        L0 = c.lanes[snap_lane];
-        has_prev = i > sg0.x;
-        has_next = i + 1 < sg0.y;
-        if (has_prev) prv = prv_;
-        const VRec nxv = has_next ? nxv_ : VRec{0.0, 0.0, 0, 0, -1, 0};
-        {
-          const int32_t sidx = me.src;
-          int2 ce = make_int2(-1, 0);
-          if (!ghost && sidx >= 0 && sidx < c.cap_rec) ce = __ldg(nrc_prev + sidx);
-          next_road = ce.x == me.rptr ? ce.y : __ldg(c.routes + me.rptr + 1);
-        }
-        v = me.v;
-        v0e_cur = py_min(p.v0, L0.cap);
-        if (L0.kind == TSB_KIND_ROAD && (L0.left >= 0 || L0.right >= 0)) {
-          mobil = true;
-          const bool any = next_road < 0;
-          mandatory = !any && conn_from_id(c, snap_lane, next_road) < 0;
-          sides0 = L0.left;
-          sides1 = L0.right;
-          if (mandatory) {
-            int32_t below = -1, above = -1;
-            for (int32_t k = c.road_lane_off[L0.road]; k < c.road_lane_off[L0.road + 1]; k++) {
-              int32_t f = c.road_lanes[k];
-              if (conn_from_id(c, f, next_road) < 0) continue;
-              if (f < snap_lane && (below < 0 || f > below)) below = f;
-              if (f > snap_lane && (above < 0 || f < above)) above = f;
-            }
-            double dl = below >= 0 ? (double)(snap_lane - below) : CUDART_INF;
-            double dr = above >= 0 ? (double)(above - snap_lane) : CUDART_INF;
-            sides0 = dl <= dr ? L0.left : L0.right;
-            sides1 = -1;
-            go = true;
-          } else {
-            const uint64_t key = c.ids_dense ? (uint64_t)me.vix : c.keys[me.vix];
-            double draw = keyed_uniform_tail(p.rng_h2, key, step_no);  // rng.py:39-41 (seed, 1, id, step)
-            go = !(draw >= p.eval_prob);
-          }
-          if (go) {
-            // a side can only win if it exists, is open and (discretionary)
-            // leads onto the next road (world.py:366-372)
-            if (sides0 >= 0 && (c.lflag[sides0] & LF_OPEN) &&
-                (mandatory || any || conn_from_id(c, sides0, next_road) >= 0))
-              my_tasks |= 1u;
-            if (sides1 >= 0 && (c.lflag[sides1] & LF_OPEN) &&
-                (mandatory || any || conn_from_id(c, sides1, next_road) >= 0))
-              my_tasks |= 2u;
-            // side-independent terms of evaluate_change (current leader, old follower)
-            const View mev{true, me.s, v};
-            const View cl = has_prev ? View{true, prv.s, prv.v} : View{false, 0.0, 0.0};
-            const View cf = has_next ? View{true, nxv.s, nxv.v} : View{false, 0.0, 0.0};
-            g_cur = gap_to(cl, me.s, Lv);
-            const double g_of_old = me.s - Lv - cf.s;
-            const double g_of_new = gap_to(cl, cf.s, Lv);
-            const bool of_ok = cf.ok && g_of_old > 0.0 && g_of_new > 0.0;
-            fr_me = idm_free<G>(p, v, v0e_cur);
-            have_fr_me = true;
-            const double a_me_x = idm_safe<G>(p, fr_me, v, dv_to(v, cl), g_cur);
-            a_me = (g_cur <= 0.0) ? -CUDART_INF : a_me_x;
-            if (my_tasks) {
-              const double fr_cf = idm_free<G>(p, cf.v, v0e_cur);
-              const double a_of_x = idm_safe<G>(p, fr_cf, cf.v, dv_to(cf.v, mev), g_of_old);
-              const double a_of_new_x = idm_safe<G>(p, fr_cf, cf.v, dv_to(cf.v, cl), g_of_new);
-              const double a_of = of_ok ? a_of_x : 0.0;
-              const double a_of_new = of_ok ? a_of_new_x : 0.0;
-              mc[tid].d_of = a_of_new - a_of;
-            }
-          }
-        }
-      }
-    }
-    if (live)
-      mc[tid] = UpdCtx{fr_me, a_me, v0e_cur, mc[tid].d_of, L0.len, next_road, sides0, sides1, snap_lane,
-                       (go ? UF_GO : 0u) | (has_prev ? UF_PREV : 0u) | (have_fr_me ? UF_FRME : 0u) |
-                           ((has_prev && g_cur >= EPS_GAP) ? UF_FINC : 0u) | (mandatory ? UF_MAND : 0u),
-                       0};
-    // list this block's side tasks (one shared atomic per warp)
-    {
-      const unsigned b0 = __ballot_sync(0xffffffffu, my_tasks & 1u);
-      const unsigned b1 = __ballot_sync(0xffffffffu, my_tasks & 2u);
-      const int ln = tid & 31;
-      __syncthreads();  // ntask reset visible
-      int wbase = 0;
-      if (ln == 0 && (b0 | b1)) wbase = atomicAdd(&ntask, __popc(b0) + __popc(b1));
-      wbase = __shfl_sync(0xffffffffu, wbase, 0);
-      const unsigned below = (1u << ln) - 1u;
-      if (my_tasks & 1u) tasks[wbase + __popc(b0 & below)] = (uint16_t)(tid << 1);
-      if (my_tasks & 2u) tasks[wbase + __popc(b0) + __popc(b1 & below)] = (uint16_t)((tid << 1) | 1);
-    }
-    __syncthreads();
-    // ---------------- phase 2: evaluate_change for every listed side
-    const int32_t nt = ntask;
-    for (int32_t t = tid; t < nt; t += UPD_BT) {
-      const int32_t tk = tasks[t];
-      const int32_t vi = tk >> 1, k = tk & 1;
-      const UpdCtx& m = mc[vi];
-      const int32_t nb = k ? m.nb1 : m.nb0;
-      const double m_s = A[base + vi].s, vv = A[base + vi].v;
-      const LaneRec LN = c.lanes[nb];
-      double ratio = 1.0;
-      if (LN.len != m.len) ratio = LN.len / m.len;
-      const double s_t = m_s * ratio;
-      const int2 sgn = seg(c, S, nb);
-      const int32_t lo = sgn.x, hi = sgn.y;
-      const int32_t mm = count_above(A, lo, hi, s_t);
-      const int32_t tl_i = mm > 0 ? lo + mm - 1 : -1;
-      const View tl = view_at(A, tl_i);
-      const View tf = view_at(A, lo + mm < hi ? lo + mm : -1);
-      const double g_tl = gap_to(tl, s_t, Lv);
-      const double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
-      const double g_nf_old = gap_to(tl, tf.s, Lv);
-      bool ok = !(g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0));
-      const double v0e_tgt = py_min(p.v0, LN.cap);
-      const double fr_me_t = (v0e_tgt == m.v0e) ? m.fr_me : idm_free<G>(p, vv, v0e_tgt);
-      const double fr_tf = idm_free<G>(p, tf.v, v0e_tgt);
-      const double a_me_new = idm_safe<G>(p, fr_me_t, vv, dv_to(vv, tl), g_tl);
-      const double a_nf_x = idm_safe<G>(p, fr_tf, tf.v, dv_to(tf.v, tl), g_nf_old);
-      const double a_nf_new_x = idm_safe<G>(p, fr_tf, tf.v, tf.v - vv, g_tf);  // new leader: me at s_t
-      const double a_nf = tf.ok ? a_nf_x : 0.0;
-      const double a_nf_new = tf.ok ? a_nf_new_x : 0.0;
-      ok = ok && !(tf.ok && a_nf_new < -p.b_safe);
-      double inc;
-      if (m.a_me == -CUDART_INF)
-        inc = CUDART_INF;
-      else
-        inc = (a_me_new - m.a_me) + p.politeness * ((a_nf_new - a_nf) + m.d_of);
-      ok = ok && ((m.flags & UF_MAND) || !(inc <= p.threshold));
-      MobRes& r = mr[k][vi];
-      r.inc = inc;
-      r.s_t = s_t;
-      r.a_new = a_me_new;
-      r.tl = tl_i;
-      r.ok = (ok ? 1 : 0) | (g_tl >= EPS_GAP ? 2 : 0);
-    }
-    __syncthreads();
-    if (!live) continue;
-    // ---------------- phase 3: choose, sense, integrate, transitions
-    {
-      const UpdCtx K = mc[tid];
-      me = A[i];
-      v = me.v;
-      fr_me = K.fr_me;
-      a_me = K.a_me;
-      v0e_cur = K.v0e;
-      next_road = K.next_road;
-      sides0 = K.nb0;
-      sides1 = K.nb1;
-      snap_lane = K.snap_lane;
-      go = K.flags & UF_GO;
-      has_prev = K.flags & UF_PREV;
-      have_fr_me = K.flags & UF_FRME;
-      g_cur = (K.flags & UF_FINC) ? EPS_GAP : 0.0;  // only compared with EPS_GAP below
-      ghost = c.sharded && i >= n_a;
-    }
-    int32_t lane = snap_lane;
-    double s = me.s;
-    bool changed = false;
-    int32_t best_tl = -1;
-    double best_a_new = 0.0;
-    bool best_gtl_ok = false;
-    double a_final = 0.0;
-    bool have_final = false;
-    if (go) {
-      bool have = false;
-      double best_inc = 0.0, best_s = 0.0;
-      int32_t best_nb = -1;
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-        if (!(my_tasks & (1u << k))) continue;
-        const MobRes& r = mr[k][tid];
-        const int32_t nb = k == 0 ? sides0 : sides1;
-        if ((r.ok & 1) && (!have || r.inc > best_inc || (r.inc == best_inc && nb < best_nb))) {
-          have = true;
-          best_inc = r.inc;
-          best_nb = nb;
-          best_s = r.s_t;
-          best_tl = r.tl;
-          best_a_new = r.a_new;
-          best_gtl_ok = r.ok & 2;
-        }
-      }
-      if (have) {
-        changed = true;
-        lane = best_nb;
-        s = best_s;
-      } else if (has_prev && g_cur >= EPS_GAP) {
-        // world.py:406 will evaluate exactly a_me: same leader (i-1), gap
-        // max(g_cur, 1e-6) == g_cur, same cap
-        a_final = a_me;
-        have_final = true;
-      }
-    }
-
-    // ---- _sense (world.py:261-317)
-    const LaneRec L1 = c.lanes[lane];  // (reloaded: not held across the block barriers)
-    double gap = CUDART_INF, lead_v = 0.0;
-    bool found = false;
-    if (!have_final) {
-      const int2 sgl = seg(c, S, lane);
-      const int32_t lo = sgl.x, hi = sgl.y;
-      if (hi > lo) {
-        int32_t ld = -1;
-        if (!changed) {
-          if (has_prev) ld = i - 1;
-        } else {
-          int32_t m = count_ahead(A, lo, hi, s, me.vix);
-          if (m > 0) ld = lo + m - 1;
-        }
-        if (ld >= 0) {
-          if (changed && ld == best_tl && best_gtl_ok) {
-            a_final = best_a_new;  // MOBIL's a_me_new: same leader, gap, cap
-            have_final = true;
-          } else {
-            gap = py_max(A[ld].s - Lv - s, EPS_GAP);
-            lead_v = A[ld].v;
-          }
-          found = true;
-        }
-      }
-    } else {
-      found = true;
-    }
-    const int32_t* roads = c.routes + me.rptr;
     if (!found) {
       const double remaining = L1.len - s;
       bool stop = false;
