@@ -126,6 +126,12 @@ typedef struct tsb_shard {
   const int32_t* export_lanes; /* own lanes in each peer's halo, ascending */
   const int32_t* import_off;   /* [nranks+1] CSR over import_lanes, by source rank */
   const int32_t* import_lanes; /* each peer's lanes in my halo, ascending */
+  /* Per export / import entry (NULL = all 0): 0 = a halo lane (its vehicles
+   * travel as ghosts); 1 = a max-pressure lane: only its post-sweep vehicle
+   * count travels (signals.py:64-86 reads it for a junction the receiver
+   * computes).  Kind-1 entries follow the kind-0 entries of their peer. */
+  const uint8_t* export_kind;
+  const uint8_t* import_kind;
 } tsb_shard;
 int tsb_create_sharded(const tsb_network* net, const tsb_trips* trips, const tsb_params* p, int32_t device,
                        const tsb_shard* shard, tsb_engine** out);

@@ -78,6 +78,7 @@ class TsbShard(C.Structure):
         ("zone", _p(C.c_uint8)),
         ("export_off", _p(C.c_int32)), ("export_lanes", _p(C.c_int32)),
         ("import_off", _p(C.c_int32)), ("import_lanes", _p(C.c_int32)),
+        ("export_kind", _p(C.c_uint8)), ("import_kind", _p(C.c_uint8)),
     ]
 
 
@@ -139,11 +140,16 @@ def pack_shard(plan) -> Packed:
         return off, _nonempty(flat, np.int32)
     eo, el = csr(plan.export_lanes)
     io, il = csr(plan.import_lanes)
+    ek = _nonempty(np.concatenate([np.asarray(x, dtype=np.uint8) for x in plan.export_kind])
+                   if plan.export_kind else np.zeros(0, np.uint8), np.uint8)
+    ik = _nonempty(np.concatenate([np.asarray(x, dtype=np.uint8) for x in plan.import_kind])
+                   if plan.import_kind else np.zeros(0, np.uint8), np.uint8)
     zone = _nonempty(plan.zone, np.uint8)
-    keep = dict(zone=zone, eo=eo, el=el, io=io, il=il)
+    keep = dict(zone=zone, eo=eo, el=el, io=io, il=il, ek=ek, ik=ik)
     s = TsbShard(rank=plan.rank, nranks=plan.nranks, zone=ptr(zone, np.uint8),
                  export_off=ptr(eo, np.int32), export_lanes=ptr(el, np.int32),
-                 import_off=ptr(io, np.int32), import_lanes=ptr(il, np.int32))
+                 import_off=ptr(io, np.int32), import_lanes=ptr(il, np.int32),
+                 export_kind=ptr(ek, np.uint8), import_kind=ptr(ik, np.uint8))
     return Packed(s, keep)
 
 

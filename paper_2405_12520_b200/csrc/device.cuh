@@ -206,6 +206,8 @@ struct Ctx {
   const int32_t* exp_peer;
   const int32_t* imp_lane;  // import entries (source-major, ascending lanes)
   const int32_t* imp_peer;
+  const uint8_t* exp_kind;  // per entry: 0 halo lane (records), 1 max-pressure lane (count only)
+  const uint8_t* imp_kind;
   int32_t* exp_cnt;
   int32_t* exp_pos;  // exclusive scan of exp_cnt (n_exp + 1)
   int32_t* imp_cnt;

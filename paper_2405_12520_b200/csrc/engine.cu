@@ -46,6 +46,7 @@ static int fail(int code, const char* fmt, ...) {
 #define SCAN_IPT_CFG 8
 #endif
 static const int SCAN_BT = 256, SCAN_IPT = SCAN_IPT_CFG, SCAN_TILE = SCAN_BT * SCAN_IPT;
+static_assert(SCAN_TILE == LANE_TILE, "k_update sums lane-scan tiles of SCAN_TILE lanes");
 
 enum KernelClass {
   KC_UPDATE,
@@ -295,6 +296,11 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
       e->cur = main_s;
     }
     cudaEventRecord(e->ev_join, e->side);
+    if (c.sharded && c.p.controller == 1) {
+      // max-pressure decisions of the previous step, from the exchanged counts
+      LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c, (int)SIG_DEFERRED);
+      LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+    }
     if (c.debug & 64) LAUNCH(KC_MISC, k_poison, 148 * 8, 256, c);
     if (c.p.pow_glibc)
       LAUNCH(KC_UPDATE, k_update<true>, grid_for(e->span, UPD_BT, UPD_GRID_CAP), UPD_BT, c);
@@ -305,9 +311,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   if (phase == 2) LAUNCH(KC_MISC, k_count_hostq, 1, 256, c);
   // bucket the post-delta state by lane, sort each lane, tentative sweep
   {
-    // two passes (tile totals, then tiles with their prefixes): no serial look-back
+    // one pass: k_update summed each tile's total (c.scan_tile_sums), so each
+    // tile adds the totals before it -- no serial look-back, no tile-sum pass
     const int ntiles = (int)(NL / SCAN_TILE + 1);
-    LAUNCH(KC_SCAN, (k_tile_sums<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, (const int32_t*)c.cnt, NL, c.scan_tile_sums);
     LAUNCH(KC_SCAN, (k_scan<SCAN_BT, SCAN_IPT>), ntiles, SCAN_BT, c, SCAN_LANES, (const int32_t*)c.cnt,
            (int32_t*)nullptr, SEL_C, (const int32_t*)nullptr, NL, ntiles, (const int32_t*)nullptr,
            (const int32_t*)c.scan_tile_sums);
@@ -323,7 +329,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     cudaStreamWaitEvent(e->side2, e->ev_fork2, 0);
     cudaStream_t main_s = e->cur;
     e->cur = e->side2;
-    LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
+    LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c, (int)SIG_FULL);
     LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
     LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);
     cudaEventRecord(e->ev_join2, e->side2);
@@ -337,8 +343,12 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
       cudaMemsetAsync(c.lane_counts, 0, sizeof(int32_t) * NL, e->cur);
       LAUNCH(KC_SIGNALS, k_lane_counts, vgrid, VB, c);
     }
-    LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c);
-    LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+    if (c.sharded && c.p.controller == 1) {
+      LAUNCH(KC_SIGNALS, k_signals, 1, 32, c, (int)SIG_CLOCK);  // decisions: next step's start
+    } else {
+      LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c, (int)SIG_FULL);
+      LAUNCH(KC_SIGNALS, k_conn_flags, cgrid, VB, c);
+    }
     LAUNCH(KC_INJECT, k_inject_due, 1, 1024, c);  // flags the step RARE when trips are due or retrying
   } else {
     cudaStreamWaitEvent(e->cur, e->ev_join2, 0);
@@ -739,6 +749,8 @@ extern "C" {
 
 const char* tsb_last_error(void) { return g_err.c_str(); }
 
+static int p_controller(const tsb_engine* e) { return e->c.p.controller; }
+
 // Sharded mode: zone flags, export/import entry lists (static per run).
 static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
   Ctx& c = e->c;
@@ -748,17 +760,26 @@ static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
   c.nranks = sh->nranks;
   RC(upload(e, (uint8_t**)&c.zone, sh->zone, NL));
   std::vector<int32_t> el, ep, il, ip;
+  std::vector<uint8_t> ek, ik;
   for (int q = 0; q < sh->nranks; q++) {
     c.peer_first_exp[q] = (int64_t)el.size();
     c.peer_first_imp[q] = (int64_t)il.size();
     for (int32_t k = sh->export_off[q]; k < sh->export_off[q + 1]; k++) {
+      const uint8_t kind = sh->export_kind ? sh->export_kind[k] : 0;
+      if (kind > 1 || (kind == 1 && p_controller(e) != 1)) return fail(TSB_EINVAL, "bad export entry kind");
+      if (!(sh->zone[sh->export_lanes[k]] & 1)) return fail(TSB_EINVAL, "export lane %d is not own", sh->export_lanes[k]);
       el.push_back(sh->export_lanes[k]);
       ep.push_back(q);
+      ek.push_back(kind);
     }
     for (int32_t k = sh->import_off[q]; k < sh->import_off[q + 1]; k++) {
-      if (!(sh->zone[sh->import_lanes[k]] & 2)) return fail(TSB_EINVAL, "import lane %d is not a halo lane", sh->import_lanes[k]);
+      const uint8_t kind = sh->import_kind ? sh->import_kind[k] : 0;
+      if (kind > 1 || (kind == 1 && p_controller(e) != 1)) return fail(TSB_EINVAL, "bad import entry kind");
+      if (kind == 0 && !(sh->zone[sh->import_lanes[k]] & 2))
+        return fail(TSB_EINVAL, "import lane %d is not a halo lane", sh->import_lanes[k]);
       il.push_back(sh->import_lanes[k]);
       ip.push_back(q);
+      ik.push_back(kind);
     }
   }
   for (int q = sh->nranks; q < 9; q++) {
@@ -771,6 +792,8 @@ static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
   RC(upload(e, (int32_t**)&c.exp_peer, ep.data(), ep.size()));
   RC(upload(e, (int32_t**)&c.imp_lane, il.data(), il.size()));
   RC(upload(e, (int32_t**)&c.imp_peer, ip.data(), ip.size()));
+  RC(upload(e, (uint8_t**)&c.exp_kind, ek.data(), ek.size()));
+  RC(upload(e, (uint8_t**)&c.imp_kind, ik.data(), ik.size()));
   RC(dalloc(e, &c.exp_cnt, el.size() + 1));
   RC(dalloc(e, &c.exp_pos, el.size() + 1));
   RC(dalloc(e, &c.imp_cnt, il.size() + 1));
@@ -786,7 +809,6 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   if (!net || !tr || !p || !out) return fail(TSB_EINVAL, "null argument");
   if (sh && (sh->nranks < 1 || sh->nranks > 8 || sh->rank < 0 || sh->rank >= sh->nranks || !sh->zone))
     return fail(TSB_EINVAL, "bad shard description (1 <= nranks <= 8)");
-  if (sh && p->controller != 0) return fail(TSB_EINVAL, "sharded mode supports fixed-time signals only");
   if (p->pow_mode != 0 && p->pow_mode != 1)
     return fail(TSB_EINVAL, "pow_mode %d unsupported (0 = correctly rounded, 1 = glibc pow)", p->pow_mode);
   // an early error return destroys the partly built engine (streams, events,
@@ -1419,6 +1441,9 @@ static int ensure_query_bufs(tsb_engine* e) {
   RC(dalloc(e, &e->q_bcnt, nb + 1));
   RC(dalloc(e, &e->q_i32, 3 * n));
   RC(dalloc(e, &e->q_f64, 3 * n));
+  // dalloc zero-fills on the legacy stream, which the engine's non-blocking
+  // stream does not wait for: finish it before the first query writes here
+  CK(cudaDeviceSynchronize());
   return TSB_OK;
 }
 

@@ -216,6 +216,11 @@ __device__ __forceinline__ int32_t count_ahead(const VRec* A, int32_t lo, int32_
   return a - lo;
 }
 
+// Lanes per tile of the step's lane scan (engine.cu SCAN_TILE): k_update adds
+// each tile's total (c.scan_tile_sums, zeroed by k_begin_step) next to the
+// per-lane counts, so the scan needs no separate tile-sum pass.
+static constexpr int LANE_TILE = 2048;
+
 // Post-update lane counts for the C layout; a vehicle that left its snapshot
 // lane is also a "mover" (k_place_movers / k_lanefix).
 // A mover's slot among its new lane's entrants comes from the same atomic
@@ -273,6 +278,8 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
   const int2* nrc_prev = c.nrc[(step_no + 1) & 1];
   int2* nrc_cur = c.nrc[step_no & 1];
   for (int32_t i = gtid(); i < n; i += gstride()) {
+    int32_t counted = -1;  // the lane this record was counted into
+    do {
     const VRec me = A[i];
     const int32_t snap_lane = me.lane;
     const bool ghost = c.sharded && i >= n_a;
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     if (i < sg0.x || i >= sg0.y || (c.sharded && !ghost && !(c.zone[snap_lane] & ZF_OWN))) {
       c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
       c.stay[i] = 0;
-      continue;
+      break;
     }
     const LaneRec L0 = c.lanes[snap_lane];
     const bool has_prev = i > sg0.x, has_next = i + 1 < sg0.y;
@@ -595,12 +602,20 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       if (!c.split) {  // closures only occur in split mode; keep the state consistent
         out.lane = nl;
         count_bucket(c, nl, snap_lane, i);
+        counted = nl;
       }
     } else {
       count_bucket(c, nl, snap_lane, i);
+      counted = nl;
       if (ghost && (c.zone[nl] & ZF_OWN)) c.status[me.vix] = TSB_STATUS_DRIVING;  // entered an own lane
     }
     c.B[i] = out;
+    } while (0);
+    // the scan's tile totals: one atomic per tile per warp
+    const unsigned am = __activemask();
+    const int32_t tile = counted >= 0 ? counted / LANE_TILE : -1;
+    const unsigned grp = __match_any_sync(am, tile);
+    if (tile >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&c.scan_tile_sums[tile], __popc(grp));
   }
 }
 
@@ -612,9 +627,10 @@ __global__ void k_count_hostq(Ctx c) {
   for (int32_t k = gtid(); k < dy->n_hostq; k += gstride()) {
     const int32_t i = c.hostq[k];
     const VRec r = c.B[i];
-    if (r.lane >= 0)
+    if (r.lane >= 0) {
       count_bucket(c, r.lane, A[i].lane, i);
-    else
+      atomicAdd(&c.scan_tile_sums[r.lane / LANE_TILE], 1);
+    } else
       c.stay[i] = 0;  // arrived during the host continuation
   }
 }
@@ -630,38 +646,15 @@ __global__ void k_count_hostq(Ctx c) {
 // blocks must be launched and draw a ticket (the gate is grid-uniform).
 static constexpr int SCAN_SITES = 6;
 enum { SCAN_LANES = 0, SCAN_INJ_LANES = 1, SCAN_INJ_RETRY = 2, SCAN_REGROUP = 3, SCAN_EXPORT = 4, SCAN_IMPORT = 5 };
-// Two-pass form for the step's lane scan: k_tile_sums writes each tile's
-// total, then k_scan (tile_sums != nullptr) takes tile b's prefix as the sum
-// of the totals before it -- no serial look-back chain across 150+ tiles.
-template <int BT, int IPT>
-__global__ void __launch_bounds__(BT) k_tile_sums(Ctx c, const int32_t* in, int32_t n, int32_t* sums) {
-  PDL_WAIT();
-  if (blockIdx.x == 0) TL_MARK(TL_SCAN);
-  const int64_t base = (int64_t)blockIdx.x * BT * IPT;
-  int32_t local = 0;
-#pragma unroll
-  for (int k = 0; k < IPT; k++) {
-    const int64_t idx = base + (int64_t)k * BT + threadIdx.x;  // coalesced
-    local += idx < n ? in[idx] : 0;
-  }
-  __shared__ int32_t s_w[BT / 32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = local;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t t = 0;
-    for (int w = 0; w < BT / 32; w++) t += s_w[w];
-    sums[blockIdx.x] = t;
-  }
-}
-
+// The step's lane scan takes the tile totals k_update summed
+// (tile_sums != nullptr): tile b's prefix is the sum of the totals before it
+// -- no serial look-back chain across 150+ tiles, no separate tile-sum pass.
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) k_scan(Ctx c, int site, const int32_t* in, int32_t* out, int out_sel,
                                              const int32_t* n_dev, int32_t n_static, int32_t ntiles,
                                              const int32_t* gate, const int32_t* tile_sums) {
   PDL_WAIT();
-  if (site == SCAN_LANES && !tile_sums) TL_MARK(TL_SCAN);
+  if (site == SCAN_LANES) TL_MARK(TL_SCAN);
   if (gated_off(gate)) return;
   int2* rng = nullptr;
   if (out_sel != SEL_NONE) {
@@ -924,6 +917,9 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
 // entered, two stayers swapped order, or the sweep would touch a vehicle
 // (world.py:531 trigger).  k_lanefix then sorts (s desc, id asc) and sweeps
 // only the flagged lanes, on chip.
+#ifndef PLACE_LIST
+#define PLACE_LIST 0  // 1: k_place appends flagged lanes to a list (atomics); 0: flag words only
+#endif
 __device__ __forceinline__ void flag_lane(const Ctx& c, int32_t L) {
   if (atomicExch(&c.fix_flag[L], 1) == 0) c.fix_list[atomicAdd(&c.dyn->n_fix, 1)] = L;
 }
@@ -943,8 +939,10 @@ __global__ void k_place(Ctx c) {
   }
   const int32_t n = dy->n_a + (c.sharded ? dy->n_g : 0);
   const int lid = threadIdx.x & 31;
+#if PLACE_LIST
   __shared__ int32_t s_cnt, s_base;
   __shared__ int32_t s_list[256];
+#endif
   // one pass in the usual case; block-uniform trip count (the block-level
   // append below synchronises), whole warps (the ballots need all 32 lanes)
   for (int32_t bbase = blockIdx.x * blockDim.x; bbase < n; bbase += gstride()) {
@@ -1005,6 +1003,7 @@ __global__ void k_place(Ctx c) {
         if (have) flag = !ahead_of(ps, pv, r.s, r.vix) || r.s > ((ps - p.L) - p.s0_floor) + 1e-12;
       }
     }
+#if PLACE_LIST
     // append newly flagged lanes: one flag atomic per lane per warp (jammed
     // lanes flag every vehicle), collected per block in shared memory, one
     // counter atomic per block (a per-warp counter atomic serialised ~30k
@@ -1024,6 +1023,16 @@ __global__ void k_place(Ctx c) {
     __syncthreads();
     for (int32_t k = threadIdx.x; k < nb; k += blockDim.x) c.fix_list[s_base + k] = s_list[k];
     __syncthreads();
+#else
+    // flag the lane for k_lanefix: a plain store per lane per warp (the flag
+    // words are the work list: k_lanefix scans them 32 lanes per warp), no
+    // atomic round trip and no block-wide append
+    const unsigned fm = __ballot_sync(0xffffffffu, flag);
+    if (flag) {
+      const unsigned grp = __match_any_sync(fm, L);
+      if (lid == __ffs(grp) - 1) c.fix_flag[L] = 1;
+    }
+#endif
   }
 }
 
@@ -1046,9 +1055,20 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const Params& p = c.p;
+#if PLACE_LIST
   const int32_t nfix = dy->n_fix;
   for (int32_t f = gtid() >> 5; f < nfix; f += warps) {
     const int32_t L = c.fix_list[f];
+#else
+  // the flagged lanes: each warp takes 32 lanes' flag words at a time
+  const int32_t ngrp = (c.n_lanes + 31) >> 5;
+  for (int32_t g = gtid() >> 5; g < ngrp; g += warps) {
+   const int32_t Lg = (g << 5) + lid;
+   unsigned todo = __ballot_sync(0xffffffffu, Lg < c.n_lanes && c.fix_flag[Lg]);
+   while (todo) {
+    const int32_t L = (g << 5) + __ffs(todo) - 1;
+    todo &= todo - 1;
+#endif
     const int32_t lo = CS[L], n = CS[L + 1] - lo;
     if (lid == 0) {
       c.fix_flag[L] = 0;
@@ -1153,6 +1173,9 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
     if (on_chip)
       for (int a = lid; a < n; a += 32) C[lo + a] = out[a];
     __syncwarp();
+#if !PLACE_LIST
+   }
+#endif
   }
 }
 
@@ -1514,11 +1537,19 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
   __shared__ int32_t lab[CL_CAP];
   __shared__ int32_t eu[CE_CAP], ev[CE_CAP];
   __shared__ int32_t indeg[CL_CAP];
-  __shared__ int32_t s_n, s_ne, s_over, s_changed, s_ncomp;
-  if (dy->rf_done) return;  // k_resolve_fast replayed the events (eager mode runs this section)
-  const int32_t ne = dy->n_events;
+  __shared__ int32_t s_n, s_ne, s_over, s_changed;
+  __shared__ int32_t s_done, s_events, s_ncl;
+  // the step scalars, read once and shared: every thread takes the same branches
+  if (threadIdx.x == 0) {
+    s_done = dy->rf_done;
+    s_events = dy->n_events;
+    s_ncl = dy->n_cl;
+  }
+  __syncthreads();
+  if (s_done) return;  // k_resolve_fast replayed the events (eager mode runs this section)
+  const int32_t ne = s_events;
   // clear the previous step's closure marks
-  for (int32_t q = threadIdx.x; q < dy->n_cl; q += blockDim.x) c.cl_idx[c.cl_lanes[q]] = 0;
+  for (int32_t q = threadIdx.x; q < s_ncl; q += blockDim.x) c.cl_idx[c.cl_lanes[q]] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     dy->n_cl = 0;
@@ -2190,11 +2221,18 @@ __global__ void k_lane_counts(Ctx c) {
 }
 
 // world.py:619-647 (+ time/step increment, world.py:677-678).
-__global__ void k_signals(Ctx c) {
+// mode SIG_FULL: both, after the step's sweep.  A sharded max-pressure engine
+// splits them: SIG_CLOCK after the sweep, SIG_DEFERRED at the start of the
+// next step, once the exchange brought the owners' post-sweep counts of the
+// pressure lanes (shard.pressure_lanes) -- the same decisions from the same
+// counts, taken before anything reads the new states (the next update).
+enum { SIG_FULL = 0, SIG_CLOCK = 1, SIG_DEFERRED = 2 };
+__global__ void k_signals(Ctx c, int mode) {
   PDL_WAIT();
   TL_MARK(TL_SIGNALS);
   const Params& p = c.p;
-  for (int32_t j = gtid(); j < c.n_junc; j += gstride()) {
+  if (mode == SIG_DEFERRED && c.dyn->step_no == 0) return;  // no step has swept yet
+  for (int32_t j = (mode == SIG_CLOCK ? c.n_junc : gtid()); j < c.n_junc; j += gstride()) {
     if (!c.junc_signal[j]) continue;
     JuncState st = c.sig[j];
     const int32_t b = c.junc_phase_off[j], np_ = c.junc_phase_off[j + 1] - b;
@@ -2235,7 +2273,7 @@ __global__ void k_signals(Ctx c) {
     }
     c.sig[j] = st;
   }
-  if (gtid() == 0) {  // world.py:677-678 (nothing in this kernel reads the clock)
+  if (gtid() == 0 && mode != SIG_DEFERRED) {  // world.py:677-678 (nothing in this kernel reads the clock)
     c.dyn->time += p.dt;
     c.dyn->step_no += 1;
   }
@@ -2651,6 +2689,7 @@ __global__ void k_speeds_done(Ctx c) {
 __global__ void k_begin_step(Ctx c) {
   PDL_WAIT();
   for (int32_t L = gtid(); L < c.n_lanes; L += gstride()) c.cnt[L] = 0;
+  for (int32_t t = gtid(); t < c.scan_tiles_cap; t += gstride()) c.scan_tile_sums[t] = 0;
   if (gtid() != 0) return;
   if (c.tl_on) c.dyn->tl_row += 1;
   TL_MARK(TL_BEGIN);
@@ -2930,7 +2969,7 @@ __global__ void k_exp_count(Ctx c, int p2p) {
   for (int32_t e = gtid(); e < c.n_exp; e += gstride()) {
     const int32_t L = c.exp_lane[e];
     const int2 sg = seg(c, S, L);
-    c.exp_cnt[e] = sg.y - sg.x;
+    c.exp_cnt[e] = c.exp_kind[e] ? 0 : sg.y - sg.x;  // a max-pressure entry carries no records
   }
 }
 
@@ -2956,7 +2995,8 @@ __global__ void k_exp_pack(Ctx c, uint8_t* send) {
     const int64_t base = exp_base(c, q);
     const int32_t L = c.exp_lane[e];
     const int32_t n = c.exp_cnt[e];
-    if (lid == 0) ((int32_t*)(send + base))[e - e0] = n;
+    // header: the lane's record count, or (max-pressure entry) its post-sweep vehicle count
+    if (lid == 0) ((int32_t*)(send + base))[e - e0] = c.exp_kind[e] ? c.lane_counts[L] : n;
     VRec* dst = (VRec*)(send + base + align32(4 * (c.peer_first_exp[q + 1] - e0))) + (c.exp_pos[e] - c.exp_pos[e0]);
     const int32_t at = seg(c, S, L).x;
     for (int32_t k = lid; k < n; k += 32) dst[k] = A[at + k];
@@ -2985,7 +3025,7 @@ __global__ void k_exp_pack_p2p(Ctx c) {
     uint8_t* base = c.p2p_peer_recv[q] + slot;
     const int32_t L = c.exp_lane[e];
     const int32_t n = c.exp_cnt[e];
-    if (lid == 0) ((int32_t*)base)[e - e0] = n;
+    if (lid == 0) ((int32_t*)base)[e - e0] = c.exp_kind[e] ? c.lane_counts[L] : n;
     VRec* dst = (VRec*)(base + align32(4 * (c.peer_first_exp[q + 1] - e0))) + (c.exp_pos[e] - c.exp_pos[e0]);
     const int32_t at = seg(c, S, L).x;
     for (int32_t k = lid; k < n; k += 32) dst[k] = A[at + k];
@@ -3042,7 +3082,13 @@ __global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
   PDL_WAIT();
   for (int32_t e = gtid(); e < c.n_imp; e += gstride()) {
     const int q = c.imp_peer[e];
-    c.imp_cnt[e] = ((const int32_t*)(recv + src_base(c, sb, q)))[e - c.peer_first_imp[q]];
+    const int32_t h = ((const int32_t*)(recv + src_base(c, sb, q)))[e - c.peer_first_imp[q]];
+    if (c.imp_kind[e]) {  // the owner's post-sweep count of a max-pressure lane
+      c.lane_counts[c.imp_lane[e]] = h;
+      c.imp_cnt[e] = 0;
+    } else {
+      c.imp_cnt[e] = h;
+    }
   }
 }
 
@@ -3057,6 +3103,7 @@ __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
   for (int32_t e = gtid() >> 5; e < c.n_imp; e += gstride() >> 5) {
     const int q = c.imp_peer[e];
     const int64_t e0 = c.peer_first_imp[q];
+    if (c.imp_kind[e]) continue;  // count only (k_imp_count)
     const int32_t L = c.imp_lane[e];
     const int32_t n = c.imp_cnt[e];
     const VRec* src = (const VRec*)(recv + src_base(c, sb, q) + align32(4 * (c.peer_first_imp[q + 1] - e0))) +

@@ -13,7 +13,16 @@
 // so every a*b+c whose product has no other use became one fused operation;
 // those contractions are restated with explicit fma() below.
 // The tables are glibc's own (pow_tables.h, extracted from libm.so.6 by
-// tools/gen_pow_tables.py).  This is not a correctly-rounded pow: it is
+// tools/gen_pow_tables.py).
+//
+// Provenance and licence: the algorithm and its constants come from glibc
+// (sysdeps/ieee754/dbl-64/e_pow.c, e_pow_log_data.c, e_exp_data.c; GNU
+// LGPL-2.1-or-later), which took them from ARM's optimized-routines
+// (Copyright (c) 2018 Arm Limited; MIT OR Apache-2.0 WITH LLVM-exception).
+// This file restates that published algorithm; the notices of both projects
+// apply to it and to pow_tables.h.
+//
+// This is not a correctly-rounded pow: it is
 // glibc's, rounding error for rounding error.  tests/test_pow_glibc.py checks
 // the host build of this file against libm on millions of arguments.
 //

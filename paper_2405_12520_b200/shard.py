@@ -40,8 +40,10 @@ class ShardPlan:
     nranks: int
     lane_owner: np.ndarray   # int32 per lane (-1 for id holes)
     zone: np.ndarray         # uint8 per lane: OWN | HALO, EXACT
-    export_lanes: list       # per destination rank: own lanes in its halo (ascending)
-    import_lanes: list       # per source rank: its lanes in my halo (ascending)
+    export_lanes: list       # per destination rank: own lanes in its halo (ascending), then pressure lanes
+    import_lanes: list       # per source rank: its lanes in my halo (ascending), then pressure lanes
+    export_kind: list = None  # per destination rank: 0 halo lane, 1 max-pressure count only
+    import_kind: list = None
 
 
 def lane_owners(flat: FlatNet, junc_pos: np.ndarray, nranks: int) -> np.ndarray:
@@ -160,16 +162,37 @@ def plan_shard(flat: FlatNet, owner: np.ndarray, rank: int, nranks: int, config)
         src = _siblings(flat, {lane}) | up({lane}, travel)
         if all(exact_update[x] for x in src if flat.lane_kind[x] >= 0):
             zone[lane] |= ZONE_EXACT
-    export_lanes, import_lanes = [], []
+    pressure = pressure_lanes(flat, zone) if getattr(config, "controller", "fixed") == "max_pressure" else set()
+    export_lanes, import_lanes, import_kind = [], [], []
     for q in range(nranks):
         if q == rank:
             export_lanes.append(np.zeros(0, dtype=np.int32))
             import_lanes.append(np.zeros(0, dtype=np.int32))
+            import_kind.append(np.zeros(0, dtype=np.uint8))
             continue
         export_lanes.append(None)
-        import_lanes.append(np.array(sorted(x for x in zone_set if owner[x] == q and zone[x] & ZONE_HALO),
-                                     dtype=np.int32))
-    return ShardPlan(rank, nranks, owner, zone, export_lanes, import_lanes)
+        halo = sorted(x for x in zone_set if owner[x] == q and zone[x] & ZONE_HALO)
+        mp = sorted(x for x in pressure if owner[x] == q)
+        import_lanes.append(np.array(halo + mp, dtype=np.int32))
+        import_kind.append(np.array([0] * len(halo) + [1] * len(mp), dtype=np.uint8))
+    return ShardPlan(rank, nranks, owner, zone, export_lanes, import_lanes, None, import_kind)
+
+
+def pressure_lanes(flat: FlatNet, zone: np.ndarray) -> set:
+    """Max-pressure sharded (signals.py:64-86, world.py:627-647): the lanes
+    whose post-sweep counts decide the phase of every junction with a
+    connector in this rank's zone (the junctions its vehicles may read): each
+    connector's predecessor and successor road lane.  Own lanes are counted
+    locally; the owners send the others' counts with every exchange, and each
+    rank advances those junctions itself at the start of the next step."""
+    conn = np.nonzero((flat.lane_kind == KIND_CONNECTOR) & (zone > 0))[0]
+    juncs = set(int(flat.lane_junction[c]) for c in conn)
+    out = set()
+    for c in np.nonzero(flat.lane_kind == KIND_CONNECTOR)[0]:
+        if int(flat.lane_junction[c]) in juncs:
+            out.add(int(flat.lane_pred1[c]))
+            out.add(int(flat.lane_succ1[c]))
+    return out
 
 
 def plan_all(flat: FlatNet, junc_pos: np.ndarray, nranks: int, config) -> list[ShardPlan]:
@@ -179,4 +202,6 @@ def plan_all(flat: FlatNet, junc_pos: np.ndarray, nranks: int, config) -> list[S
     for r, p in enumerate(plans):
         p.export_lanes = [plans[q].import_lanes[r] if q != r else np.zeros(0, dtype=np.int32)
                           for q in range(nranks)]
+        p.export_kind = [plans[q].import_kind[r] if q != r else np.zeros(0, dtype=np.uint8)
+                         for q in range(nranks)]
     return plans

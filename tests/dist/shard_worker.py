@@ -22,6 +22,8 @@ from paper_2405_12520_b200.sharded import ShardedWorld  # noqa: E402
 
 SCEN = {
     "grid6x2": lambda: (generate_grid(6, 6, lanes_per_direction=2), 1500, 3, (0.0, 300.0)),
+    "grid6x2mp": lambda: (generate_grid(6, 6, lanes_per_direction=2), 2500, 3, (0.0, 300.0)),
+    "grid8x3mp": lambda: (generate_grid(8, 8, lanes_per_direction=3), 4000, 9, (0.0, 400.0)),
     "dense": lambda: (generate_grid(6, 6, block_length=80.0, lanes_per_direction=2), 5000, 5, (0.0, 200.0)),
     "grid8x3": lambda: (generate_grid(8, 8, lanes_per_direction=3), 4000, 9, (0.0, 400.0)),
 }
@@ -98,10 +100,11 @@ def check_queries(sw, ref, rank, k) -> int:
     rng = np.random.default_rng(k)
     ids = ref._ft.ids
     for i in rng.choice(len(ids), min(25, len(ids)), replace=False).tolist():
-        if sw.get_vehicle(ids[i]) != ref.get_vehicle(ids[i]):
-            print(f"rank {rank} step {k}: get_vehicle({ids[i]}) differs", flush=True)
+        got = sw.get_vehicle(ids[i])  # collective: every rank makes every call
+        if got != ref.get_vehicle(ids[i]):
+            print(f"rank {rank} step {k}: get_vehicle({ids[i]}) differs: {got} vs {ref.get_vehicle(ids[i])}",
+                  flush=True)
             bad += 1
-            break
     return bad
 
 
@@ -115,7 +118,7 @@ def main():
         return
     rank, ws = dist.get_rank(), dist.get_world_size()
     net, trips, seed = scenario(name)
-    cfg = EngineConfig()
+    cfg = EngineConfig(controller="max_pressure") if name.endswith("mp") else EngineConfig()
     sw = ShardedWorld.from_network(net, trips, cfg, seed=seed, rank=rank, nranks=ws, device=0, host_staging=True,
                                    p2p=p2p)
     ref = World(net, trips, cfg, seed=seed)

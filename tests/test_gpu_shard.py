@@ -43,6 +43,17 @@ def test_sharded_p2p_equals_single(name, steps, nproc, port):
     assert "p2p_used=1" in _run(name, steps, nproc, port, "p2p")
 
 
+@pytest.mark.parametrize("name,steps,nproc,port,mode", [("grid6x2mp", 300, 2, 29651, ""),
+                                                        ("grid8x3mp", 200, 3, 29652, "p2p")])
+def test_sharded_max_pressure(name, steps, nproc, port, mode):
+    """Max-pressure signals sharded (signals.py:64-86): each rank advances the
+    junctions its vehicles may read at the start of the next step, from its own
+    lanes' post-sweep counts and the owners' counts of the other pressure
+    lanes (shard.pressure_lanes), exchanged with the ghosts -- own lanes,
+    every counter and the merged queries equal the single engine's."""
+    _run(name, steps, nproc, port, mode)
+
+
 def test_sharded_p2p_fallback_when_a_rank_cannot_map():
     """A rank that cannot map its peers makes every rank fall back to the
     collective transport; results unchanged."""

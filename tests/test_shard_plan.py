@@ -66,6 +66,38 @@ def test_export_import_lists_are_mutual():
                 assert np.all(plans[q].zone[imp] & shard.ZONE_HALO)
 
 
+@pytest.mark.parametrize("n", [2, 3])
+def test_max_pressure_lanes_are_counted_or_imported(n):
+    """Max-pressure sharded: for every junction with a connector in a rank's
+    zone, each connector's predecessor and successor lane is own (counted
+    locally) or imported from its owner as a count-only entry (kind 1); the
+    owner's export list mirrors it, and fixed-time plans carry no such entries."""
+    net = generate_grid(6, 6, lanes_per_direction=2)
+    flat = flatten_network(net, "max_pressure")
+    jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    plans = shard.plan_all(flat, jp, n, EngineConfig(controller="max_pressure"))
+    fixed = shard.plan_all(flat, jp, n, EngineConfig())
+    for p, pf in zip(plans, fixed):
+        assert all(not np.any(k) for k in pf.import_kind)
+        conn = np.nonzero((flat.lane_kind == KIND_CONNECTOR) & (p.zone > 0))[0]
+        juncs = set(flat.lane_junction[conn].tolist())
+        need = set()
+        for c in np.nonzero(flat.lane_kind == KIND_CONNECTOR)[0]:
+            if flat.lane_junction[c] in juncs:
+                need |= {int(flat.lane_pred1[c]), int(flat.lane_succ1[c])}
+        got = set()
+        for q in range(n):
+            lanes, kinds = p.import_lanes[q], p.import_kind[q]
+            assert np.all(np.diff(kinds.astype(int)) >= 0)  # kind-1 entries follow the halo lanes
+            mp = lanes[kinds == 1]
+            assert np.all(p.lane_owner[mp] == q)
+            got |= set(mp.tolist())
+            assert np.array_equal(plans[q].export_lanes[p.rank], lanes)
+            assert np.array_equal(plans[q].export_kind[p.rank], kinds)
+        own = {x for x in need if p.lane_owner[x] == p.rank}
+        assert need == own | got and not (own & got)
+
+
 def test_ring_two_ranks():
     net = make_ring(40, radius=40 * 200.0 / (2 * math.pi))
     flat, plans = _plans(net, 2)
