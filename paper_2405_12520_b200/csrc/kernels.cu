@@ -918,7 +918,7 @@ __global__ void k_lanesort(Ctx c, int dst_sel, const int32_t* gate) {
 // (world.py:531 trigger).  k_lanefix then sorts (s desc, id asc) and sweeps
 // only the flagged lanes, on chip.
 #ifndef PLACE_LIST
-#define PLACE_LIST 0  // 1: k_place appends flagged lanes to a list (atomics); 0: flag words only
+#define PLACE_LIST 1  // 1: k_place appends flagged lanes to a list (atomics); 0: flag words only (same speed, A/B r2)
 #endif
 __device__ __forceinline__ void flag_lane(const Ctx& c, int32_t L) {
   if (atomicExch(&c.fix_flag[L], 1) == 0) c.fix_list[atomicAdd(&c.dyn->n_fix, 1)] = L;
