@@ -142,6 +142,7 @@ struct Params {
   double inv_ab2;    // 1 / sqrt_ab2 when sqrt_ab2 is a power of two (then x / sqrt_ab2 == x * inv_ab2 exactly)
   int32_t ab2_pow2;
   double rcp_ab2;    // RN(1 / sqrt_ab2): x / sqrt_ab2 by div_rcp()
+  double rcp_v0;     // RN(1 / v0): v / v0 by div_rcp() (0: plain division)
   uint64_t rng_h2;   // keyed-RNG fold state after (seed, STREAM_MOBIL): constant for the run
   int32_t controller;
   int32_t delta_int; // delta as an integer power if integral in [1, 64], else 0
@@ -340,6 +341,10 @@ __device__ __forceinline__ double pow4_cr(double x) {
   return h + l;
 }
 
+#ifndef UPD_RCPV0
+#define UPD_RCPV0 1
+#endif
+
 // x / b for a divisor fixed for the run, given y = RN(1/b): q = RN(x*y) is
 // within one ulp of x/b, the residual x - b*q is exact (FMA), and
 // RN(q + r*y) is the correctly rounded quotient (Markstein's theorem) as
@@ -360,7 +365,13 @@ __device__ __forceinline__ double div_rcp(double x, double b, double y) {
 // carries the code of its own mode).
 template <bool G>
 __device__ __forceinline__ double idm_free(const Params& p, double v, double v0_eff) {
+#if UPD_RCPV0
+  // v0_eff == v0 (the lane's cap is not lower): the correctly rounded
+  // quotient by the run constant's reciprocal (div_rcp), else the division
+  const double x = (v0_eff == p.v0 && p.rcp_v0 != 0.0) ? div_rcp(v, p.v0, p.rcp_v0) : div_pos(v, v0_eff);
+#else
   const double x = div_pos(v, v0_eff);
+#endif
   if (G) return glibc_pow::pow(x, p.delta);
   if (p.delta_int == 4) return pow4_cr(x);  // the default delta (params.py)
   return p.delta_int ? pow_int_cr(x, p.delta_int) : pow(x, p.delta);

@@ -319,7 +319,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
            (const int32_t*)c.scan_tile_sums);
   }
   LAUNCH(KC_PLACE, k_place, vgrid, VB, c);
-  LAUNCH(KC_LANEFIX, k_lanefix, 148 * 8, 32 * LX_WARPS, c);
+  LAUNCH(KC_LANEFIX, k_lanefix, 148 * LX_BLOCKS_PER_SM, 32 * LX_WARPS, c);
   // Fixed-time signals, the clock and the due list do not depend on vehicle
   // positions: with a fixed-time controller they run on a parallel branch
   // beside the revert resolution (joined before the injection section).
@@ -879,6 +879,11 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
     // div_rcp needs a divisor whose reciprocal is a normal number with room
     // to spare; 0 selects the plain division
     P.rcp_ab2 = (std::isfinite(P.sqrt_ab2) && P.sqrt_ab2 > 0.0 && std::abs(ex) < 500) ? 1.0 / P.sqrt_ab2 : 0.0;
+    // the free-road ratio v / v0_eff divides by v0 itself whenever the lane's
+    // cap is not lower (every lane of the synthetic grids): same scheme
+    int ex0 = 0;
+    std::frexp(p->idm_v0, &ex0);
+    P.rcp_v0 = (std::isfinite(p->idm_v0) && p->idm_v0 > 0.0 && std::abs(ex0) < 500) ? 1.0 / p->idm_v0 : 0.0;
     auto mix = [](uint64_t z) {
       z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           const double g_tf = tf.ok ? s_t - Lv - tf.s : CUDART_INF;
           const double g_nf_old = gap_to(tl, tf.s, Lv);
           ok = ok && !(g_tl <= 0.0 || g_tf <= 0.0 || (tf.ok && g_nf_old <= 0.0));
-          const double v0e_tgt = py_min(p.v0, LN.cap);
+                    const double v0e_tgt = py_min(p.v0, LN.cap);
           const double fr_me_t = (v0e_tgt == v0e_cur) ? fr_me : idm_free<G>(p, v, v0e_tgt);
           const double fr_tf = idm_free<G>(p, tf.v, v0e_tgt);
           const double a_me_new = idm_safe<G>(p, fr_me_t, v, dv_to(v, tl), g_tl);
@@ -1041,6 +1041,11 @@ __global__ void k_place(Ctx c) {
 #endif
 static constexpr int LX_CAP = LX_CAP_CFG;  // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
+// k_lanefix grid: blocks per SM (grid-stride over the flagged lanes); 5 is
+// what fits at once (shared memory), so the launch is one full wave
+#ifndef LX_BLOCKS_PER_SM
+#define LX_BLOCKS_PER_SM 8
+#endif
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_LANEFIX);
@@ -1646,11 +1651,15 @@ __global__ void __launch_bounds__(1024) k_resolve_closure(Ctx c) {
       }
     }
     __syncthreads();
+    // pointer jumping in two phases (walk, then publish): no thread writes a
+    // label another thread may be walking through
     for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
       int32_t x = lab[i];
       while (lab[x] != x) x = lab[x];
-      lab[i] = x;
+      indeg[i] = x;
     }
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) lab[i] = indeg[i];
     __syncthreads();
     if (!s_changed) break;
     __syncthreads();
