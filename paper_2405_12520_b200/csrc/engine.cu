@@ -107,6 +107,7 @@ struct tsb_engine {
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   cudaEvent_t marks[8] = {};
   cudaGraph_t body_graph = nullptr;
+  bool body_first = false;  // the next launch opens a conditional body (engine.cu LAUNCH)
   bool capturing = false;
   cudaError_t capture_err = cudaSuccess;
   int32_t launches_per_step = 0;
@@ -178,10 +179,11 @@ struct Launcher {
 // Launched with programmatic stream serialization (PDL, see kernels.cu
 // PDL_WAIT): the next kernel's launch overlaps the previous kernel's tail.
 template <class... KArgs, class... Args>
-static void launch_pdl(cudaStream_t st, int prio, dim3 grid, dim3 block, void (*kern)(KArgs...), Args&&... args) {
+static void launch_pdl(cudaStream_t st, int prio, bool pdl, dim3 grid, dim3 block, void (*kern)(KArgs...),
+                       Args&&... args) {
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   attr[1].id = cudaLaunchAttributePriority;
   attr[1].val.priority = prio;
   cudaLaunchConfig_t cfg = {};
@@ -202,10 +204,13 @@ static int side_prio(const tsb_engine* e) {
   return (e->cur == e->side || e->cur == e->side2) ? e->prio_hi : 0;
 }
 
+// The first kernel of a conditional body has no predecessor inside the body
+// graph: it is launched without the programmatic-serialization attribute.
 #define LAUNCH(kc, kern, grid, block, ...)                          \
   do {                                                              \
     L.pre(kc);                                                      \
-    launch_pdl(e->cur, side_prio(e), dim3(grid), dim3(block), kern, __VA_ARGS__); \
+    launch_pdl(e->cur, side_prio(e), !e->body_first, dim3(grid), dim3(block), kern, __VA_ARGS__); \
+    e->body_first = false;                                          \
     L.post();                                                       \
   } while (0)
 
@@ -243,6 +248,7 @@ static void cond_begin(tsb_engine* e, int k) {
   }
   if (er != cudaSuccess && e->capture_err == cudaSuccess) e->capture_err = er;
   e->cur = e->body;
+  e->body_first = true;
 }
 static void cond_end(tsb_engine* e) {
   if (!e->capturing || !e->c.use_cond) return;

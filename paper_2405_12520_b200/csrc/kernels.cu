@@ -177,6 +177,35 @@ struct View {
   double s, v;
 };
 
+// B (the post-update records) is written once by k_update and read once by
+// k_place: with REC_STREAM its lines are marked evict-first in L2
+// (st.global.cs / ld.global.cs) so they do not push the snapshot and the lane
+// tables out of the 126 MB L2.
+#ifndef REC_STREAM
+#define REC_STREAM 0
+#endif
+__device__ __forceinline__ void store_b(VRec* p, const VRec& r) {
+#if REC_STREAM
+  const double2* src = reinterpret_cast<const double2*>(&r);
+  double2* dst = reinterpret_cast<double2*>(p);
+  __stcs(dst, src[0]);
+  __stcs(dst + 1, src[1]);
+#else
+  *p = r;
+#endif
+}
+__device__ __forceinline__ VRec load_b(const VRec* p) {
+#if REC_STREAM
+  VRec r;
+  double2* d = reinterpret_cast<double2*>(&r);
+  d[0] = __ldcs(reinterpret_cast<const double2*>(p));
+  d[1] = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+  return r;
+#else
+  return *p;
+#endif
+}
+
 __device__ __forceinline__ View view_at(const VRec* A, int32_t k) {
   if (k < 0) return View{false, 0.0, 0.0};
   return View{true, A[k].s, A[k].v};
@@ -292,7 +321,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     const VRec nxv_ = A[i + 1 < n ? i + 1 : i];
     const int2 sg0 = seg(c, S, snap_lane);
     if (i < sg0.x || i >= sg0.y || (c.sharded && !ghost && !(c.zone[snap_lane] & ZF_OWN))) {
-      c.B[i] = VRec{me.s, me.v, me.vix, me.rptr, -1, i};
+      store_b(&c.B[i], VRec{me.s, me.v, me.vix, me.rptr, -1, i});
       c.stay[i] = 0;
       break;
     }
@@ -609,7 +638,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
       counted = nl;
       if (ghost && (c.zone[nl] & ZF_OWN)) c.status[me.vix] = TSB_STATUS_DRIVING;  // entered an own lane
     }
-    c.B[i] = out;
+    store_b(&c.B[i], out);
     } while (0);
     // the scan's tile totals: one atomic per tile per warp
     const unsigned am = __activemask();
@@ -949,7 +978,7 @@ __global__ void k_place(Ctx c) {
     const int32_t base = bbase + (threadIdx.x & ~31);
     const int32_t j = base + lid;
     const bool valid = j < n;
-    const VRec r = valid ? c.B[j] : VRec{0.0, 0.0, 0, 0, -1, 0};
+    const VRec r = valid ? load_b(&c.B[j]) : VRec{0.0, 0.0, 0, 0, -1, 0};
     const bool st = valid && c.stay[j];
     const unsigned stay_bits = __ballot_sync(0xffffffffu, st);
     const int32_t L = r.lane;
