@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 T=g8
-VARIANTS="base spec base_m3 spec_m3" sh profiles/abv.sh > gpurun_out/${T}_ab.txt 2>&1; echo ab rc $?
+VARIANTS="base spec base_m3 spec_m3" sh profiles/round2/abv.sh > gpurun_out/${T}_ab.txt 2>&1; echo ab rc $?
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""; [ $tool = memcheck ] && extra="--leak-check full"; [ $tool = racecheck ] && extra="--racecheck-report hazard"
   timeout 1500 compute-sanitizer --tool $tool $extra --error-exitcode 9 python tools/sanitize_run.py 200 8 > gpurun_out/${T}_${tool}_gated.log 2>&1; echo $tool gated rc $?
