@@ -182,7 +182,7 @@ struct View {
 // (st.global.cs / ld.global.cs) so they do not push the snapshot and the lane
 // tables out of the 126 MB L2.
 #ifndef REC_STREAM
-#define REC_STREAM 0
+#define REC_STREAM 1
 #endif
 __device__ __forceinline__ void store_b(VRec* p, const VRec& r) {
 #if REC_STREAM
@@ -339,7 +339,11 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
     {
       const int32_t sidx = me.src;
       int2 ce = make_int2(-1, 0);
+#if REC_STREAM
+      if (!ghost && sidx >= 0 && sidx < c.cap_rec) ce = __ldcs(nrc_prev + sidx);  // last read of the cache entry
+#else
       if (!ghost && sidx >= 0 && sidx < c.cap_rec) ce = __ldg(nrc_prev + sidx);
+#endif
       next_road = ce.x == me.rptr ? ce.y : __ldg(roads + 1);
     }
     const double v = me.v;
@@ -1073,7 +1077,7 @@ static constexpr int LX_WARPS = 8;
 // k_lanefix grid: blocks per SM (grid-stride over the flagged lanes); 5 is
 // what fits at once (shared memory), so the launch is one full wave
 #ifndef LX_BLOCKS_PER_SM
-#define LX_BLOCKS_PER_SM 8
+#define LX_BLOCKS_PER_SM 5
 #endif
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   PDL_WAIT();
