@@ -247,6 +247,28 @@ int tsb_signal_state(tsb_engine* e, int32_t* phase, double* elapsed);
 int tsb_route(tsb_engine* e, int32_t origin, int32_t dest, int32_t cap, int32_t* lanes,
               int32_t* n, double* cost);
 
+/* Native grid builder (host only, no device): the flattened arrays of
+ * trafficsim's generate_grid(rows, cols, block_length, lanes_per_direction,
+ * max_speed) compiled by build_network (network.py:367-560) -- the same lane
+ * numbering, geometry and signal programs -- without Python objects.
+ * tsb_grid_sizes: sizes[0..9] = lanes, successors, predecessors, roads, road
+ * lanes, junctions, phases, geometry segments, bytes of the '\n'-joined road
+ * ids, bytes of the junction ids.  tsb_grid_export copies into 28 caller
+ * buffers, in this order (NULL skips one): lane_len, lane_cap, lane_kind,
+ * lane_open, lane_left, lane_right, lane_road, lane_junction, lane_pred1,
+ * lane_succ1, succ_off, succ, pred_off, pred, road_lane_off, road_lanes,
+ * junc_signal, junc_phase_off, phase_dur, lane_green_mask, junc_phase0,
+ * junc_elapsed0, geo_off (int64), geo_cum, geo_angle, junction positions
+ * (x, y per junction), road ids, junction ids. */
+typedef struct tsb_grid tsb_grid;
+int tsb_grid_build(int32_t rows, int32_t cols, double block_length, int32_t lanes_per_direction,
+                   double max_speed, int32_t controller, tsb_grid** out);
+int tsb_grid_sizes(const tsb_grid* g, int64_t* sizes);
+int tsb_grid_export(const tsb_grid* g, void* const* dst);
+void tsb_grid_destroy(tsb_grid* g);
+/* CPython's math.dist for two points (the grid builder's lengths; test hook). */
+double tsb_py_dist(double ax, double ay, double bx, double by);
+
 /* Standalone router (no device): used by demand generators and tests. */
 typedef struct tsb_router tsb_router;
 int tsb_router_create(const tsb_network* net, tsb_router** out);

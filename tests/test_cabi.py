@@ -28,7 +28,8 @@ def declared_symbols():
 def test_header_declares_the_surface():
     syms = declared_symbols()
     for s in ("tsb_create", "tsb_step", "tsb_state", "tsb_destroy", "tsb_last_error", "tsb_road_acc",
-              "tsb_min_front_gap", "tsb_set_lane", "tsb_set_signal_phase", "tsb_finished", "tsb_status"):
+              "tsb_min_front_gap", "tsb_set_lane", "tsb_set_signal_phase", "tsb_finished", "tsb_status",
+              "tsb_get_vehicles", "tsb_records", "tsb_set_geometry", "tsb_grid_build", "tsb_grid_export"):
         assert s in syms
 
 
