@@ -38,8 +38,9 @@ sys.path.insert(0, ROOT)
 B_ALG = 60  # bytes per vehicle-update: r+w {id,lane,road_pos,s,v} + route gather
 # fp64 flops per vehicle-update in k_update (dadd + dmul + 2 x dfma thread
 # instructions of one launch / vehicles), from the ncu --set full capture
-FP64_FLOP_PER_UPDATE = 392.0
-FP64_FLOP_SOURCE = "ncu --set full of k_update<false> on M1 (profiles/r2a_k_update_ncu_summary.txt)"
+FP64_FLOP_PER_UPDATE = 387.0
+FP64_FLOP_SOURCE = ("ncu --set full of one k_update<false> launch on M1: dadd + dmul + 2 x dfma thread instructions "
+                    "/ vehicles (profiles/round2/k_update_fp64.json)")
 METRIC = "vehicle-updates/sec"
 UNIT = "vehicle-updates/s"
 
@@ -52,7 +53,7 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False):
+def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False, rows: int = 100):
     """M1/C4 inputs -> (net or None, FlatNet, trips, FlatTrips, junction positions).
 
     GPU arm: the native grid builder (csrc/gridgen.cpp, pinned by sha256 to
@@ -69,7 +70,7 @@ def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False)
         from oracle.bind import OracleRouter
         from paper_2405_12520_b200 import generate_grid
 
-        net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
+        net = generate_grid(rows, 100, block_length=400.0, lanes_per_direction=3)
         flat = flatten_network(net)
         jpos = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
         router = OracleRouter(net, flat=flat)
@@ -78,7 +79,7 @@ def build_workload(n_vehicles: int, spacing: float, oracle_router: bool = False)
         from paper_2405_12520_b200.gridgen import grid_flat
 
         net = None
-        flat, jpos = grid_flat(100, 100, block_length=400.0, lanes_per_direction=3)
+        flat, jpos = grid_flat(rows, 100, block_length=400.0, lanes_per_direction=3)
         router = Router(None, flat=flat)
     trips = preplaced_trips(flat if net is None else net, router, n_vehicles, spacing)
     router.close()
@@ -120,7 +121,12 @@ def run_sharded(args, ws, rank, local, pg, workload):
     from paper_2405_12520_b200 import EngineConfig, _native
     from paper_2405_12520_b200.sharded import ShardedWorld
 
-    net, flat, trips, ft, jp = build_workload(args.vehicles, args.spacing)
+    # strong scaling (default): the same 1M-vehicle M1 network split N ways;
+    # --weak: N x 1M vehicles on a (100 N) x 100 grid -- each band of 100
+    # junction rows is an M1-sized block, so per-GPU work is fixed
+    rows = 100 * ws if args.weak else 100
+    n_total = args.vehicles * ws if args.weak else args.vehicles
+    net, flat, trips, ft, jp = build_workload(n_total, args.spacing, rows=rows)
     p2p = args.exchange == "p2p"
     sw = ShardedWorld(flat, ft, jp, EngineConfig(), 42, rank, ws, device=local,
                       host_staging=os.environ.get("TSB_BENCH_GLOO") == "1", p2p=p2p)
@@ -163,8 +169,10 @@ def run_sharded(args, ws, rank, local, pg, workload):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "vehicles_total": args.vehicles, "lanes": flat.n_lanes,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": (f"{n_total} pre-placed routable vehicles on generate_grid({rows},100,400 m,3 lanes), "
+                                f"{args.vehicles} per GPU" if args.weak else workload),
+                   "vehicles_total": n_total, "lanes": flat.n_lanes,
                    "parallelism": f"lane bands x{ws} (sharded.py; halo lanes rank0: {halo} vs own {own})",
                    "exchange": ("per step: pack kernel writes boundary-lane packets into the peers' "
                                 "IPC-mapped receive slots (NVLink P2P), release/acquire flags, ghost import; "
@@ -365,6 +373,8 @@ def main():
     ap.add_argument("--cpu-warm-steps", type=int, default=11)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--debug", type=int, default=0, help="tsb_set_debug flags (experiments; results unchanged)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: weak scaling, --vehicles per GPU on a (100 N) x 100 grid (default: strong, M1 split N ways)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: device-driven exchange over peer memory, or NCCL all-to-all")
     ap.add_argument("--pow", default="correct", choices=["correct", "glibc"],

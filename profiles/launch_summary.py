@@ -5,7 +5,7 @@ hdr = None; data = []
 for r in rows:
     if r and r[0] == 'ID': hdr = r; continue
     if hdr and len(r) == len(hdr): data.append(dict(zip(hdr, r)))
-seq = [(d['Kernel Name'].split('(')[0], float(d['Metric Value'])) for d in data if d['Metric Name'] == 'gpu__time_duration.sum']
+seq = [(d['Kernel Name'].split('(')[0].replace('void ', '').replace('tsb::', ''), float(d['Metric Value'])) for d in data if d['Metric Name'] == 'gpu__time_duration.sum']
 idx = [i for i, (k, v) in enumerate(seq) if k.startswith('k_update') or k.startswith('void k_update')]
 a = idx[first]; b = idx[first + steps]
 agg = collections.defaultdict(float); cnt = collections.Counter()
