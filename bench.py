@@ -542,8 +542,9 @@ def main():
                    "sequential_resolve_steps": r_end.resolve_sequential, "steps_total": r_end.step_no},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": sync_bytes.value,
-                "how": "World.step() loop (reference API), wall clock; each step synchronises and reads the "
-                       "step scalars (StepReport counters + error flags) back to the host; a stateful "
+                "how": "World.step() loop (reference API), wall clock; each step waits for and reads the "
+                       "step scalars (StepReport counters + error flags), which the step's last block writes "
+                       "into mapped host memory (zero-copy D2H); a stateful "
                        "simulator: inputs were uploaded once at construction, as the reference's bench "
                        "(cli.py:482-489) times steps without a recorder"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

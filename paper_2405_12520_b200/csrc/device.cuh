@@ -278,6 +278,10 @@ struct Ctx {
   int32_t* hostq;
   Dyn* dyn;
   unsigned long long* tl;  // step timestamps, TL_ROWS x TL_SLOTS (kernels.cu TL_MARK)
+  // end-of-step report published into mapped (zero-copy) host memory by the
+  // block that ends the step: the step scalars, then the step number
+  Dyn* pub_dyn;
+  volatile long long* pub_seq;
   int32_t tl_on;           // tsb_set_timeline
   double* scratch_d;
 };

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -117,6 +118,8 @@ struct tsb_engine {
   int32_t* q_i32 = nullptr;
   double* q_f64 = nullptr;
   bool loc_valid = false;  // q_loc describes the current snapshot
+  uint8_t* pub_host = nullptr;  // mapped: the published Dyn, then the step number (c.pub_dyn / c.pub_seq)
+  int64_t steps_issued = 0;     // steps enqueued so far (== the device step number once they ran)
   int64_t q_cap = 0;       // tsb_get_vehicles query capacity
   uint8_t* q_dev = nullptr;
   uint8_t* q_host = nullptr;
@@ -720,6 +723,7 @@ static int build_graph(tsb_engine* e) {
 static int do_steps(tsb_engine* e, int32_t n) {
   e->loc_valid = false;
   if (n <= 0) return TSB_OK;
+  e->steps_issued += n;
   RC(ensure_windows(e, n));
   if (e->routes_stale) {
     RC(route_pending(e, false));
@@ -1116,6 +1120,14 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   RC(dalloc(E, &c.dyn, 1));
   RC(dalloc(E, &c.scratch_d, 16));
   CK(cudaMallocHost((void**)&e->dyn_host, sizeof(Dyn)));
+  if (!sh) {  // single engine: the step report is published into mapped host memory
+    CK(cudaHostAlloc((void**)&e->pub_host, sizeof(Dyn) + 64, cudaHostAllocMapped));
+    memset(e->pub_host, 0, sizeof(Dyn) + 64);
+    uint8_t* dptr = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&dptr, e->pub_host, 0));
+    c.pub_dyn = reinterpret_cast<Dyn*>(dptr);
+    c.pub_seq = reinterpret_cast<volatile long long*>(dptr + sizeof(Dyn) + 32 - (sizeof(Dyn) % 32));
+  }
   for (int q = 0; q < 2 * 96; q++) CK(cudaEventCreate(&e->ev[q]));
   memset(e->dyn_host, 0, sizeof(Dyn));
   c.n_win = 0;
@@ -1295,6 +1307,7 @@ void tsb_destroy(tsb_engine* e) {
   for (void* p : e->allocs) cudaFree(p);
   if (e->q_dev) cudaFree(e->q_dev);
   if (e->q_host) cudaFreeHost(e->q_host);
+  if (e->pub_host) cudaFreeHost(e->pub_host);
   if (e->dyn_host) cudaFreeHost(e->dyn_host);
   if (e->stream) cudaStreamDestroy(e->stream);
   if (e->body) cudaStreamDestroy(e->body);
@@ -1328,12 +1341,57 @@ static void fill_report(const tsb_engine* e, tsb_report* r) {
   r->reverts_total = d.reverts_total;
 }
 
+static inline unsigned long long host_mix64(unsigned long long z) {  // kernels.cu mix64
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// After a step graph: the report the step's last block published into mapped
+// host memory (no copy node, no stream synchronisation on the common path).
+// Spins on the published step number, checking the stream now and then;
+// falls back to sync_dyn if the publication does not come (eager and split
+// modes, or an error).
+static int wait_published(tsb_engine* e) {
+  const long long target = e->steps_issued;
+  const volatile long long* seq = reinterpret_cast<const volatile long long*>(
+      e->pub_host + sizeof(Dyn) + 32 - (sizeof(Dyn) % 32));
+  // the device writes the scalars, then the step number and their hash, with
+  // no ordering between them: accept a copy whose hash matches
+  auto consistent = [&]() -> bool {
+    if (seq[0] < target) return false;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    std::memcpy(e->dyn_host, e->pub_host, sizeof(Dyn));
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(e->dyn_host);
+    unsigned long long h = 0x9E3779B97F4A7C15ULL;
+    for (size_t k = 0; k < sizeof(Dyn) / 8; k++) h = host_mix64(h ^ w[k]);
+    return e->dyn_host->step_no == target && (long long)h == seq[1];
+  };
+  bool ok = false;
+  for (long spins = 0; !(ok = consistent()); spins++) {
+    if ((spins & 1023) == 1023) {
+      const cudaError_t q = cudaStreamQuery(e->stream);
+      if (q == cudaSuccess) {  // the stream drained: the writes have landed (or never came)
+        ok = consistent();
+        break;
+      }
+      if (q != cudaErrorNotReady) return sync_dyn(e);
+    }
+  }
+  if (!ok) return sync_dyn(e);
+  if (e->dyn_host->overflow) return sync_dyn(e);  // (re-reads, reports the flag)
+  return TSB_OK;
+}
+
 int tsb_step(tsb_engine* e, int32_t n_steps, tsb_report* last) {
   if (!e) return fail(TSB_EINVAL, "null engine");
   if (n_steps < 0) return fail(TSB_EINVAL, "steps must be non-negative");
   CK(cudaSetDevice(e->device));
   RC(do_steps(e, n_steps));
-  RC(sync_dyn(e));
+  if (e->pub_host && n_steps > 0 && !e->c.split && !e->profiling)
+    RC(wait_published(e));
+  else
+    RC(sync_dyn(e));
   if (last) fill_report(e, last);
   return TSB_OK;
 }
@@ -1783,7 +1841,7 @@ int tsb_fp64_peak(int32_t device, double* tflops) {
 
 int tsb_step_sync_bytes(int64_t* n) {
   if (!n) return fail(TSB_EINVAL, "null argument");
-  *n = (int64_t)sizeof(Dyn);
+  *n = (int64_t)sizeof(Dyn) + 16;  // the published step scalars + step number + hash (mapped host memory)
   return TSB_OK;
 }
 
