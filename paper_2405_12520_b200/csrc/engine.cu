@@ -1363,8 +1363,8 @@ static int wait_published(tsb_engine* e) {
     std::atomic_thread_fence(std::memory_order_acquire);
     std::memcpy(e->dyn_host, e->pub_host, sizeof(Dyn));
     const unsigned long long* w = reinterpret_cast<const unsigned long long*>(e->dyn_host);
-    unsigned long long h = 0x9E3779B97F4A7C15ULL;
-    for (size_t k = 0; k < sizeof(Dyn) / 8; k++) h = host_mix64(h ^ w[k]);
+    unsigned long long h = 0;  // kernels.cu regroup_finish
+    for (size_t k = 0; k < sizeof(Dyn) / 8; k++) h ^= host_mix64(w[k] + 0x9E3779B97F4A7C15ULL * (k + 1));
     return e->dyn_host->step_no == target && (long long)h == seq[1];
   };
   bool ok = false;

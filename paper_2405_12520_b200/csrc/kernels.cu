@@ -2595,18 +2595,24 @@ __device__ void regroup_finish(const Ctx& c) {
     dy->fin_log_n += dy->finished_now;
     dy->speeds_pending = 1;  // accumulated by the next step's k_speeds branch or a flush
     dy->n_own = 0;           // sharded: recounted by k_count_own
-    if (c.pub_dyn) {
-      // the step's scalars into mapped host memory, then the step number and
-      // a hash of the scalars: tsb_step waits for the number and accepts the
-      // copy once the hash matches (no system fence on the step's critical path)
-      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(dy);
-      unsigned long long* dst = reinterpret_cast<unsigned long long*>(c.pub_dyn);
-      unsigned long long h = 0x9E3779B97F4A7C15ULL;
-      for (int k = 0; k < (int)(sizeof(Dyn) / 8); k++) {
-        const unsigned long long w = src[k];
-        dst[k] = w;
-        h = mix64(h ^ w);
-      }
+  }
+  if (c.pub_dyn && threadIdx.x < 32) {
+    // the step's scalars into mapped host memory by one warp, then the step
+    // number and an order-free hash of the scalars: tsb_step waits for the
+    // number and accepts the copy once the hash matches (plain stores: no
+    // system fence on the step's critical path)
+    __syncwarp();
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(dy);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(c.pub_dyn);
+    unsigned long long h = 0;
+    for (int k = threadIdx.x; k < (int)(sizeof(Dyn) / 8); k += 32) {
+      const unsigned long long w = src[k];
+      dst[k] = w;
+      h ^= mix64(w + 0x9E3779B97F4A7C15ULL * (unsigned long long)(k + 1));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+    if (threadIdx.x == 0) {
       c.pub_seq[0] = dy->step_no;
       c.pub_seq[1] = (long long)h;
     }
