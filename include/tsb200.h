@@ -135,6 +135,16 @@ typedef struct tsb_shard {
 } tsb_shard;
 int tsb_create_sharded(const tsb_network* net, const tsb_trips* trips, const tsb_params* p, int32_t device,
                        const tsb_shard* shard, tsb_engine** out);
+/* The same with the rank's zone renumbered into a compact local lane space
+ * (shard.local_network): `local_net` holds only the rank's lanes (own, halo,
+ * max-pressure lanes) with local ids, local_to_global[local] = global id
+ * (ascending, so every lane-id order and tie-break is unchanged), `shard`
+ * uses local ids, the trips global ids; routes are computed on `global_net`
+ * (the road ids of a route are global in both).  Every lane-proportional
+ * buffer and kernel of the rank shrinks to its zone. */
+int tsb_create_sharded_local(const tsb_network* global_net, const tsb_network* local_net,
+                             const int32_t* local_to_global, const tsb_trips* trips, const tsb_params* p,
+                             int32_t device, const tsb_shard* shard, tsb_engine** out);
 /* After a step: pack the boundary lanes for every peer into `send` (device
  * memory of `cap` bytes); bytes[q] = size of the message to rank q. */
 int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes);

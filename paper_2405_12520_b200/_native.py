@@ -60,6 +60,7 @@ SIGNATURES = {
     "tsb_fp64_peak": (_i32, [_i32, C.POINTER(_f64)]),
     "tsb_step_sync_bytes": (_i32, [C.POINTER(_i64)]),
     "tsb_create_sharded": (_i32, [_vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
+    "tsb_create_sharded_local": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _vp, C.POINTER(_vp)]),
     "tsb_mark": (_i32, [_vp, _i32]),
     "tsb_set_pow_mode": (_i32, [_vp, _i32]),
     "tsb_marks_elapsed": (_i32, [_vp, _i32, _i32, C.POINTER(_f64)]),

@@ -73,6 +73,7 @@ struct tsb_engine {
   std::vector<void*> allocs;
   // host copies (authoritative for control changes and host continuation)
   int32_t n_lanes = 0, n_roads = 0, n_junc = 0, n_trips = 0;
+  int32_t n_lanes_global = 0;  // the whole network's lanes (== n_lanes unless a shard is renumbered locally)
   int32_t n_pend = 0;  // trips this engine injects (all, or the shard's own)
   int64_t cap = 0;     // record capacity of the vehicle layouts (engine.cu create_impl)
   int64_t span = 1;    // records the one-pass vehicle grids are sized for
@@ -84,6 +85,7 @@ struct tsb_engine {
   std::vector<uint8_t> junc_signal;
   std::vector<VCold> cold;
   std::vector<int32_t> dest;
+  std::vector<int32_t> origin_global;  // trips' origin lanes as global ids (local lane numbering only)
   std::unique_ptr<Router> router;
   std::vector<std::vector<int32_t>> route_host;  // roads_seq per vix
   int64_t pool_used = 0, pool_cap = 0;
@@ -490,7 +492,7 @@ static int route_pending(tsb_engine* e, bool all) {
   for (int32_t k = 0; k < e->n_trips; k++)
     if (all || (!routed[k] && status[k] == TSB_STATUS_WAITING)) {
       idx.push_back(k);
-      org.push_back(e->cold[k].origin_lane);
+      org.push_back(e->origin_global.empty() ? e->cold[k].origin_lane : e->origin_global[k]);
       dst.push_back(e->dest[k]);
     }
   if (idx.empty()) return TSB_OK;
@@ -814,9 +816,15 @@ static int setup_shard(tsb_engine* e, const tsb_shard* sh) {
   return TSB_OK;
 }
 
+// route_net / l2g (sharded, local lane numbering): `net` holds only the
+// rank's local lanes (l2g[local] = global id, ascending), routes come from
+// the whole network route_net, and the trips' lanes are global ids.
 static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_params* p, int32_t device,
-                       const tsb_shard* sh, tsb_engine** out) {
+                       const tsb_shard* sh, tsb_engine** out, const tsb_network* route_net = nullptr,
+                       const int32_t* l2g = nullptr) {
   if (!net || !tr || !p || !out) return fail(TSB_EINVAL, "null argument");
+  if ((route_net != nullptr) != (l2g != nullptr) || (route_net && !sh))
+    return fail(TSB_EINVAL, "local lane numbering needs the whole network, the lane map and a shard");
   if (sh && (sh->nranks < 1 || sh->nranks > 8 || sh->rank < 0 || sh->rank >= sh->nranks || !sh->zone))
     return fail(TSB_EINVAL, "bad shard description (1 <= nranks <= 8)");
   if (p->pow_mode != 0 && p->pow_mode != 1)
@@ -848,6 +856,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   e->cur = e->stream;
   e->c.p2p_timeout_ns = 60ULL * 1000000000ULL;
   const int32_t NL = e->n_lanes = net->n_lanes;
+  e->n_lanes_global = route_net ? route_net->n_lanes : NL;
   const int32_t NR = e->n_roads = net->n_roads;
   const int32_t NJ = e->n_junc = net->n_junctions;
   const int32_t N = e->n_trips = tr->n;
@@ -953,6 +962,18 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   for (int32_t j = 0; j < NJ; j++) sig[j] = JuncState{net->junc_phase0[j], 0, net->junc_elapsed0[j], 0.0};
 
   // trips
+  // global -> local lane ids (local numbering), else the identity
+  std::vector<int32_t> g2l;
+  if (l2g) {
+    g2l.assign(route_net->n_lanes, -1);
+    for (int32_t l = 0; l < NL; l++) {
+      if (l2g[l] < 0 || l2g[l] >= route_net->n_lanes || (l > 0 && l2g[l] <= l2g[l - 1]))
+        return fail(TSB_EINVAL, "local lane map must be ascending global ids");
+      g2l[l2g[l]] = l;
+    }
+    e->origin_global.assign(tr->origin_lane, tr->origin_lane + N);
+  }
+  auto local_of = [&](int32_t g) { return l2g ? (g >= 0 && g < (int32_t)g2l.size() ? g2l[g] : -1) : g; };
   e->cold.resize(N);
   e->dest.resize(N);
   e->route_host.resize(N);
@@ -962,7 +983,7 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
     cd.key = tr->key[k];
     cd.route_off = 0;
     cd.route_len = -1;
-    cd.origin_lane = tr->origin_lane[k];
+    cd.origin_lane = local_of(tr->origin_lane[k]);  // -1: outside the rank's lanes (never injected here)
     cd.origin_s = tr->origin_s[k];
     cd.depart = tr->departure[k];
     e->dest[k] = tr->dest_lane[k];
@@ -970,18 +991,27 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   }
   if (sh) {  // a rank injects the trips whose origin lane it owns
     pend.erase(std::remove_if(pend.begin(), pend.end(),
-                              [&](int32_t k) { return !(sh->zone[tr->origin_lane[k]] & 1); }),
+                              [&](int32_t k) {
+                                const int32_t o = local_of(tr->origin_lane[k]);
+                                return o < 0 || !(sh->zone[o] & 1);
+                              }),
                pend.end());
   }
   std::stable_sort(pend.begin(), pend.end(), [&](int32_t a, int32_t b) {
     return tr->departure[a] < tr->departure[b];  // ties keep ascending id
   });
   const int32_t NP = e->n_pend = c.n_pend = (int32_t)pend.size();
+  // a shard's one-pass grids cover its own trips plus as many ghosts (the
+  // kernels stride over anything beyond): not the whole fleet's 2N
+  if (sh) e->span = std::min<int64_t>(e->span, 2 * (int64_t)NP + N / 16 + 1024);
   std::vector<double> pend_dep(NP);
   for (int32_t k = 0; k < NP; k++) pend_dep[k] = tr->departure[pend[k]];
 
-  e->router = std::make_unique<Router>(NL, net->lane_kind, net->lane_len, net->lane_cap, net->lane_open,
-                                       net->succ_off, net->succ, net->pred_off, net->pred, net->lane_road);
+  {
+    const tsb_network* rn = route_net ? route_net : net;  // routes over the whole network
+    e->router = std::make_unique<Router>(rn->n_lanes, rn->lane_kind, rn->lane_len, rn->lane_cap, rn->lane_open,
+                                         rn->succ_off, rn->succ, rn->pred_off, rn->pred, rn->lane_road);
+  }
 
   // device uploads
   tsb_engine* E = e.get();
@@ -1009,6 +1039,10 @@ static int create_impl(const tsb_network* net, const tsb_trips* tr, const tsb_pa
     std::vector<int2> span(NR);
     for (int32_t r = 0; r < NR; r++) {
       const int32_t a = net->road_lane_off[r], b = net->road_lane_off[r + 1];
+      if (b <= a && l2g) {  // a road outside the rank's local lanes
+        span[r] = make_int2(0, -1);
+        continue;
+      }
       if (b <= a) return fail(TSB_EINVAL, "road %d has no lanes", r);
       for (int32_t q = a + 1; q < b; q++)
         if (net->road_lanes[q] != net->road_lanes[q - 1] + 1)
@@ -1161,6 +1195,13 @@ int tsb_create_sharded(const tsb_network* net, const tsb_trips* tr, const tsb_pa
   return create_impl(net, tr, p, device, sh, out);
 }
 
+int tsb_create_sharded_local(const tsb_network* global_net, const tsb_network* local_net, const int32_t* local_to_global,
+                             const tsb_trips* tr, const tsb_params* p, int32_t device, const tsb_shard* sh,
+                             tsb_engine** out) {
+  if (!global_net || !local_to_global || !sh) return fail(TSB_EINVAL, "null argument");
+  return create_impl(local_net, tr, p, device, sh, out, global_net, local_to_global);
+}
+
 int tsb_shard_export(tsb_engine* e, void* send, int64_t cap, int64_t* bytes) {
   if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");
   Ctx& c = e->c;
@@ -1218,7 +1259,9 @@ int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_
   CK(cudaSetDevice(e->device));
   if (!c.p2p_flag) {
     // a slot holds one peer's message: per-lane counts (<= every lane) + records (<= every vehicle)
-    c.p2p_slot = (((int64_t)4 * e->n_lanes + 31) & ~(int64_t)31) + (int64_t)32 * std::max(e->n_trips, 1) + 64;
+    // (the same on every rank: it is also the stride the peers write with --
+    // sized by the whole network's lane count, not this rank's local lanes)
+    c.p2p_slot = (((int64_t)4 * e->n_lanes_global + 31) & ~(int64_t)31) + (int64_t)32 * std::max(e->n_trips, 1) + 64;
     uint8_t* r = nullptr;
     unsigned long long* f = nullptr;
     CK(cudaMalloc((void**)&r, (size_t)(2 * c.nranks) * (size_t)c.p2p_slot));

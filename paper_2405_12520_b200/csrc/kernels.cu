@@ -160,7 +160,8 @@ __device__ __forceinline__ void write_conn_flags(const Ctx& c, int32_t j, const 
   for (int32_t q = c.jc_off[j]; q < c.jc_off[j + 1]; q++) {
     const int32_t cn = c.jc[q];
     uint8_t f = c.lflag[cn] & LF_OPEN;
-    if (c.lflag[c.lanes[cn].succ1] & LF_OPEN) f |= LF_SUCC_OPEN;
+    const int32_t sc = c.lanes[cn].succ1;  // < 0: outside a sharded rank's local lanes
+    if (sc >= 0 && (c.lflag[sc] & LF_OPEN)) f |= LF_SUCC_OPEN;
     f |= (uint8_t)(aspect_of(c, j, cn, st) << LF_ASPECT_SHIFT);
     c.lflag[cn] = f;
   }
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
           } else {
             nxt = LC.succ1;
             rq += 1;
-            if (!(c.lflag[nxt] & LF_OPEN)) break;
+            if (nxt < 0 || !(c.lflag[nxt] & LF_OPEN)) break;  // (< 0: beyond a rank's local lanes)
           }
           const int2 sgx = seg(c, S, nxt);
           const int32_t lo = sgx.x, hi = sgx.y;
@@ -605,6 +606,11 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         nl = conn;
         LT = c.lanes[conn];
       } else {
+        if (LT.succ1 < 0) {  // a sharded rank's halo edge: the lane beyond is not local (inexact zone)
+          ns = LT.len;
+          nv = 0.0;
+          break;
+        }
         ns -= LT.len;
         nl = LT.succ1;
         nptr += 1;
@@ -2297,7 +2303,8 @@ __global__ void k_signals(Ctx c, int mode) {
             int32_t cn = c.jc[q];
             if ((c.green[cn] >> ph) & 1ULL) {
               const LaneRec LR = c.lanes[cn];
-              pr += (long long)c.lane_counts[LR.pred1] - (long long)c.lane_counts[LR.succ1];
+              if (LR.pred1 >= 0 && LR.succ1 >= 0)  // (a sharded rank's junction it never reads may be partial)
+                pr += (long long)c.lane_counts[LR.pred1] - (long long)c.lane_counts[LR.succ1];
             }
           }
           if (!have || pr > best_p) {
@@ -2327,7 +2334,7 @@ __global__ void k_conn_flags(Ctx c) {
   for (int32_t q = gtid(); q < c.n_conn; q += gstride()) {
     const int32_t cn = c.jc[q], j = c.jc_junc[q];
     uint8_t f = c.lflag[cn] & LF_OPEN;
-    if (c.lflag[c.jc_succ1[q]] & LF_OPEN) f |= LF_SUCC_OPEN;
+    if (c.jc_succ1[q] >= 0 && (c.lflag[c.jc_succ1[q]] & LF_OPEN)) f |= LF_SUCC_OPEN;
     f |= (uint8_t)(aspect_of(c, j, cn, c.sig[j]) << LF_ASPECT_SHIFT);
     c.lflag[cn] = f;
   }
@@ -3177,7 +3184,11 @@ __global__ void k_imp_copy(Ctx c, const uint8_t* recv, SrcBase sb) {
       continue;
     }
     if (lid == 0) c.rng[dy->cur][L] = make_int2(at, at + n);
-    for (int32_t k = lid; k < n; k += 32) A[at + k] = src[k];
+    for (int32_t k = lid; k < n; k += 32) {
+      VRec r = src[k];
+      r.lane = L;  // the sender's lane id in this rank's numbering (local lane spaces differ)
+      A[at + k] = r;
+    }
   }
   if (gtid() == 0) dy->n_g = c.imp_pos[c.n_imp];
 }

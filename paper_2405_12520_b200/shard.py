@@ -205,3 +205,73 @@ def plan_all(flat: FlatNet, junc_pos: np.ndarray, nranks: int, config) -> list[S
         p.export_kind = [plans[q].import_kind[r] if q != r else np.zeros(0, dtype=np.uint8)
                          for q in range(nranks)]
     return plans
+
+
+def local_network(flat: FlatNet, plan: ShardPlan):
+    """The rank's zone as a compact local lane space (tsb_create_sharded_local).
+
+    Local lanes are the rank's own and halo lanes, the max-pressure lanes it
+    counts or imports, and their roads' sibling lanes, in ascending global id
+    (l2g is increasing, so every lane-id comparison -- MOBIL ties, the sweep
+    order, revert chains -- is unchanged).  Lane references that leave the
+    local set (a halo lane's successors at the zone edge) become -1; roads and
+    junctions keep their global indices (routes are sequences of global road
+    ids).  Returns (local FlatNet, l2g, local ShardPlan)."""
+    from dataclasses import replace
+
+    n = flat.n_lanes
+    keep = set(np.nonzero(plan.zone > 0)[0].tolist())
+    for lists in (plan.import_lanes, plan.export_lanes):
+        for x in lists:
+            keep.update(int(v) for v in x)
+    keep = _siblings(flat, keep)
+    l2g = np.array(sorted(keep), dtype=np.int32)
+    g2l = np.full(n, -1, dtype=np.int32)
+    g2l[l2g] = np.arange(len(l2g), dtype=np.int32)
+
+    def remap(a):
+        a = np.asarray(a)
+        out = np.full(a.shape, -1, dtype=np.int32)
+        ok = a >= 0
+        out[ok] = g2l[a[ok]]
+        return out
+
+    def csr(off, idx):
+        lists = [remap(idx[off[g]:off[g + 1]]) for g in l2g]
+        lists = [x[x >= 0] for x in lists]
+        o = np.zeros(len(l2g) + 1, dtype=np.int32)
+        o[1:] = np.cumsum([len(x) for x in lists]) if len(lists) else []
+        v = np.concatenate(lists).astype(np.int32) if lists else np.zeros(0, np.int32)
+        return o, v
+
+    succ_off, succ = csr(flat.succ_off, flat.succ)
+    pred_off, pred = csr(flat.pred_off, flat.pred)
+    nr = len(flat.road_ids)
+    rl = [remap(flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]]) for r in range(nr)]
+    rl = [x[x >= 0] for x in rl]
+    road_lane_off = np.zeros(nr + 1, dtype=np.int32)
+    road_lane_off[1:] = np.cumsum([len(x) for x in rl])
+    road_lanes = np.concatenate(rl).astype(np.int32) if rl else np.zeros(0, np.int32)
+    nseg = (flat.geo_off[l2g + 1] - flat.geo_off[l2g]).astype(np.int64)
+    geo_off = np.zeros(len(l2g) + 1, dtype=np.int64)
+    geo_off[1:] = np.cumsum(nseg)
+    seg_idx = np.concatenate([np.arange(flat.geo_off[g], flat.geo_off[g + 1]) for g in l2g]) if len(l2g) \
+        else np.zeros(0, np.int64)
+    lflat = replace(
+        flat, n_lanes=len(l2g),
+        lane_len=flat.lane_len[l2g].copy(), lane_cap=flat.lane_cap[l2g].copy(),
+        lane_kind=flat.lane_kind[l2g].copy(), lane_open=flat.lane_open[l2g].copy(),
+        lane_left=remap(flat.lane_left[l2g]), lane_right=remap(flat.lane_right[l2g]),
+        lane_road=flat.lane_road[l2g].copy(), lane_junction=flat.lane_junction[l2g].copy(),
+        lane_pred1=remap(flat.lane_pred1[l2g]), lane_succ1=remap(flat.lane_succ1[l2g]),
+        succ_off=succ_off, succ=succ, pred_off=pred_off, pred=pred,
+        road_lane_off=road_lane_off, road_lanes=road_lanes,
+        lane_green_mask=flat.lane_green_mask[l2g].copy(),
+        geo_off=geo_off, geo_cum=flat.geo_cum[seg_idx].copy(), geo_angle=flat.geo_angle[seg_idx].copy(),
+    )
+    lplan = ShardPlan(plan.rank, plan.nranks, plan.lane_owner[l2g].copy(), plan.zone[l2g].copy(),
+                      [remap(x) for x in plan.export_lanes], [remap(x) for x in plan.import_lanes],
+                      plan.export_kind, plan.import_kind)
+    for x in lplan.export_lanes + lplan.import_lanes:
+        assert np.all(x >= 0), "an exchange lane is outside the local lane set"
+    return lflat, l2g, lplan

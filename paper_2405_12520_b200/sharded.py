@@ -75,7 +75,7 @@ class ShardedWorld:
 
     def __init__(self, flat: FlatNet, ft: FlatTrips, junc_pos: np.ndarray, config: EngineConfig | None,
                  seed: int, rank: int, nranks: int, device: int = 0, group=None, host_staging: bool = False,
-                 pow_mode: int = 1, p2p: bool = False):
+                 pow_mode: int = 1, p2p: bool = False, local_lanes: bool = True):
         import torch
         import torch.distributed as dist
 
@@ -88,15 +88,30 @@ class ShardedWorld:
         self.host_staging = host_staging
         self.flat, self.ft = flat, ft
         self.plan = shard.plan_all(flat, junc_pos, nranks, self.config)[rank]
-        pn, pt, ps = pack_network(flat), pack_trips(ft), pack_shard(self.plan)
+        pn, pt = pack_network(flat), pack_trips(ft)
         params = pack_params(self.config, seed, pow_mode=pow_mode)
         h = C.c_void_p()
-        _native.check(_native.lib().tsb_create_sharded(C.byref(pn.struct), C.byref(pt.struct), C.byref(params),
-                                                       device, C.byref(ps.struct), C.byref(h)))
+        self.local_lanes = local_lanes
+        if local_lanes:
+            # the rank's zone renumbered into a compact local lane space: every
+            # lane-proportional buffer and kernel of the rank shrinks to it
+            lflat, self.l2g, lplan = shard.local_network(flat, self.plan)
+            pl, ps = pack_network(lflat), pack_shard(lplan)
+            l2g = np.ascontiguousarray(self.l2g, dtype=np.int32)
+            _native.check(_native.lib().tsb_create_sharded_local(
+                C.byref(pn.struct), C.byref(pl.struct), l2g.ctypes.data, C.byref(pt.struct), C.byref(params),
+                device, C.byref(ps.struct), C.byref(h)))
+            self._eng_zone, gflat = lplan.zone, lflat
+        else:
+            ps = pack_shard(self.plan)
+            _native.check(_native.lib().tsb_create_sharded(C.byref(pn.struct), C.byref(pt.struct), C.byref(params),
+                                                           device, C.byref(ps.struct), C.byref(h)))
+            self.l2g = np.arange(flat.n_lanes, dtype=np.int32)
+            self._eng_zone, gflat = self.plan.zone, flat
         self._h = h
-        geo_off = np.ascontiguousarray(flat.geo_off, dtype=np.int64)
-        geo_cum = np.ascontiguousarray(flat.geo_cum if len(flat.geo_cum) else np.zeros(1), dtype=np.float64)
-        geo_ang = np.ascontiguousarray(flat.geo_angle if len(flat.geo_angle) else np.zeros(1), dtype=np.float64)
+        geo_off = np.ascontiguousarray(gflat.geo_off, dtype=np.int64)
+        geo_cum = np.ascontiguousarray(gflat.geo_cum if len(gflat.geo_cum) else np.zeros(1), dtype=np.float64)
+        geo_ang = np.ascontiguousarray(gflat.geo_angle if len(gflat.geo_angle) else np.zeros(1), dtype=np.float64)
         _native.check(_native.lib().tsb_set_geometry(h, geo_off.ctypes.data, int(geo_off[-1]),
                                                      geo_cum.ctypes.data, geo_ang.ctypes.data))
         self._report = TsbReport()
@@ -174,12 +189,13 @@ class ShardedWorld:
 
     @classmethod
     def from_network(cls, net, trips, config=None, seed=0, rank=0, nranks=1, device=0, group=None,
-                     host_staging=False, p2p=False):
+                     host_staging=False, p2p=False, local_lanes=True):
         config = config or EngineConfig()
         flat = flatten_network(net, config.controller)
         ft = flatten_trips(flat, trips)
         jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64).reshape(-1, 2)
-        return cls(flat, ft, jp, config, seed, rank, nranks, device, group, host_staging, p2p=p2p)
+        return cls(flat, ft, jp, config, seed, rank, nranks, device, group, host_staging, p2p=p2p,
+                   local_lanes=local_lanes)
 
     def close(self):
         if self._h is not None:
@@ -250,7 +266,7 @@ class ShardedWorld:
         """This rank's own vehicles, lane-sorted: dict of arrays (vix, lane, road_pos, s, v)."""
         n = max(len(self.ft.ids), 1)
         nd = C.c_int32()
-        ls = np.zeros(self.flat.n_lanes + 1, dtype=np.int32)
+        ls = np.zeros(len(self.l2g) + 1, dtype=np.int32)
         out = {k: np.zeros(2 * n, dtype=t) for k, t in (("vix", np.int32), ("lane", np.int32),
                                                          ("road_pos", np.int32), ("s", np.float64),
                                                          ("v", np.float64))}
@@ -258,8 +274,10 @@ class ShardedWorld:
                                               out["lane"].ctypes.data, out["road_pos"].ctypes.data,
                                               out["s"].ctypes.data, out["v"].ctypes.data))
         m = nd.value
-        own = (self.plan.zone[out["lane"][:m]] & shard.ZONE_OWN) > 0
-        return {k: a[:m][own] for k, a in out.items()}
+        own = (self._eng_zone[out["lane"][:m]] & shard.ZONE_OWN) > 0
+        res = {k: a[:m][own] for k, a in out.items()}
+        res["lane"] = self.l2g[res["lane"]]  # global lane ids (ascending map: the lane-major order holds)
+        return res
 
     # ------------------------------------------------------------ queries (collective: every rank calls)
     #
@@ -288,7 +306,10 @@ class ShardedWorld:
         q = np.array([k], dtype=np.int32)
         o = np.zeros(1, dtype=VIEW_DTYPE)
         _native.check(_native.lib().tsb_get_vehicles(self._h, q.ctypes.data, 1, o.ctypes.data))
-        views = self._gather(o[0].tolist())
+        mine = list(o[0].tolist())
+        if mine[5] in (1, 2):
+            mine[3] = int(self.l2g[mine[3]])  # this rank's local lane id -> global
+        views = self._gather(tuple(mine))
         pick = next((v for v in views if v[5] in (1, 2, 3)), views[0])  # driving, finished, dropped
         s, v, fin, lane, rp, st, _ = pick
         status = _STATUS[st] if st >= 0 else _STATUS[0]
@@ -311,7 +332,9 @@ class ShardedWorld:
         _native.check(_native.lib().tsb_records(self._h, n, *(bufs[k].ctypes.data for k in
                                                             ("vix", "lane", "road_pos", "s", "v", "angle_deg")),
                                                 C.byref(m)))
-        parts = self._gather({k: a[:m.value] for k, a in bufs.items()})
+        mine = {k: a[:m.value] for k, a in bufs.items()}
+        mine["lane"] = self.l2g[mine["lane"]].astype(np.int32)  # global lane ids
+        parts = self._gather(mine)
         out = {k: np.concatenate([p[k] for p in parts]) for k in bufs}
         order = np.argsort(out["vix"], kind="stable")
         out = {k: a[order] for k, a in out.items()}

@@ -120,7 +120,7 @@ def main():
     net, trips, seed = scenario(name)
     cfg = EngineConfig(controller="max_pressure") if name.endswith("mp") else EngineConfig()
     sw = ShardedWorld.from_network(net, trips, cfg, seed=seed, rank=rank, nranks=ws, device=0, host_staging=True,
-                                   p2p=p2p)
+                                   p2p=p2p, local_lanes=os.environ.get("TSB_SHARD_GLOBAL_LANES") != "1")
     ref = World(net, trips, cfg, seed=seed)
     own_zone = sw.plan.zone
     bad = 0

@@ -54,6 +54,13 @@ def test_sharded_max_pressure(name, steps, nproc, port, mode):
     _run(name, steps, nproc, port, mode)
 
 
+@pytest.mark.parametrize("name,steps,nproc,port", [("grid8x3", 150, 3, 29661), ("dense", 150, 2, 29662)])
+def test_sharded_global_lane_numbering(name, steps, nproc, port):
+    """The sharded engine on the whole network's lane numbering (no local
+    renumbering, tsb_create_sharded): same result as the single engine."""
+    _run(name, steps, nproc, port, env={"TSB_SHARD_GLOBAL_LANES": "1"})
+
+
 def test_sharded_p2p_fallback_when_a_rank_cannot_map():
     """A rank that cannot map its peers makes every rank fall back to the
     collective transport; results unchanged."""

@@ -98,6 +98,39 @@ def test_max_pressure_lanes_are_counted_or_imported(n):
         assert need == own | got and not (own & got)
 
 
+@pytest.mark.parametrize("controller", ["fixed", "max_pressure"])
+def test_local_lane_space(controller):
+    """shard.local_network: the rank's lanes in ascending global order; own and
+    halo lanes, exchange lanes and whole roads present; every own lane keeps
+    all of its successors and predecessors (only the zone edge loses any);
+    lane references and exchange lists map back to the global ids."""
+    net = generate_grid(8, 8, lanes_per_direction=3)
+    flat = flatten_network(net, controller)
+    jp = np.array([net.junctions[j].position for j in flat.junction_ids], dtype=np.float64)
+    for p in shard.plan_all(flat, jp, 3, EngineConfig(controller=controller)):
+        lf, l2g, lp = shard.local_network(flat, p)
+        assert np.all(np.diff(l2g) > 0) and lf.n_lanes == len(l2g) < flat.n_lanes
+        assert set(np.nonzero(p.zone > 0)[0].tolist()) <= set(l2g.tolist())
+        assert np.array_equal(lp.zone, p.zone[l2g])
+        for q in range(p.nranks):
+            assert np.array_equal(l2g[lp.import_lanes[q]], p.import_lanes[q])
+            assert np.array_equal(l2g[lp.export_lanes[q]], p.export_lanes[q])
+        for r in range(len(lf.road_ids)):
+            mine = lf.road_lanes[lf.road_lane_off[r]:lf.road_lane_off[r + 1]]
+            full = flat.road_lanes[flat.road_lane_off[r]:flat.road_lane_off[r + 1]]
+            assert len(mine) in (0, len(full)) and np.array_equal(l2g[mine], full[:len(mine)])
+        for l in np.nonzero(lp.zone & shard.ZONE_OWN)[0]:
+            g = l2g[l]
+            for off, idx, loff, lidx in ((flat.succ_off, flat.succ, lf.succ_off, lf.succ),
+                                         (flat.pred_off, flat.pred, lf.pred_off, lf.pred)):
+                assert np.array_equal(l2g[lidx[loff[l]:loff[l + 1]]], idx[off[g]:off[g + 1]])
+        for k in ("lane_left", "lane_right", "lane_pred1", "lane_succ1"):
+            a, b = getattr(lf, k), getattr(flat, k)[l2g]
+            ok = a >= 0
+            assert np.array_equal(l2g[a[ok]], b[ok])
+        assert np.array_equal(lf.lane_len, flat.lane_len[l2g])
+
+
 def test_ring_two_ranks():
     net = make_ring(40, radius=40 * 200.0 / (2 * math.pi))
     flat, plans = _plans(net, 2)
