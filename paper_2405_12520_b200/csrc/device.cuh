@@ -129,6 +129,7 @@ struct Dyn {
   int32_t pad4_;
   unsigned long long xchg_epoch;  // sharded P2P exchanges so far (k_exp_count)
   unsigned long long xchg_bytes;  // sharded P2P: bytes this rank wrote into peer slots so far
+  unsigned long long xchg_packed; // sharded P2P: blocks of k_exp_pack_signal finished so far (all launches)
   // cumulative step-path counters (tsb_path_counters)
   int64_t n_resolve_fast, n_resolve_general, n_regroup_patch, n_regroup_full, n_inject_steps;
 };

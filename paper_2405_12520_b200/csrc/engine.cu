@@ -263,25 +263,21 @@ static void cond_end(tsb_engine* e) {
 }
 
 // Sharded engine with mapped peers: the ghost exchange over peer memory
-// (kernels.cu k_exp_pack_p2p), the epoch kept on the device so the sequence
+// (kernels.cu k_exp_prep .. k_imp_copy), the epoch kept on the device so the sequence
 // can be part of the step graph.
 static void issue_exchange(tsb_engine* e, Launcher& L) {
   Ctx& c = e->c;
   const int VB = 256;
-  LAUNCH(KC_MISC, k_exp_count, grid_for(std::max(c.n_exp, 1), VB, 1 << 20), VB, c, 1);
-  if (c.n_exp > 0) {
-    scan(e, L, KC_MISC, SCAN_EXPORT, c.exp_cnt, c.exp_pos, SEL_NONE, nullptr, c.n_exp, c.n_exp, nullptr);
-    LAUNCH(KC_MISC, k_exp_pack_p2p, grid_for((int64_t)c.n_exp * 32, VB, 1 << 20), VB, c);
-  }
-  LAUNCH(KC_MISC, k_p2p_signal, 1, 32, c);
-  LAUNCH(KC_MISC, k_p2p_wait, 1, 32, c);
-  if (c.n_imp > 0) {
-    SrcBase sb{};
-    sb.b[0] = -1;  // slots of the current epoch (kernels.cu src_base)
-    LAUNCH(KC_MISC, k_imp_count, grid_for(c.n_imp, VB, 1 << 20), VB, c, (const uint8_t*)e->p2p_recv, sb);
-    scan(e, L, KC_MISC, SCAN_IMPORT, c.imp_cnt, c.imp_pos, SEL_NONE, nullptr, c.n_imp, c.n_imp, nullptr);
+  SrcBase sb{};
+  sb.b[0] = -1;  // slots of the current epoch (kernels.cu src_base)
+  // four kernels: counts + scan, own count + pack + flag release, wait +
+  // import counts + scan, copy (kernels.cu k_exp_prep ... k_imp_copy)
+  LAUNCH(KC_MISC, k_exp_prep, 1, 1024, c);
+  const int64_t pw = std::max<int64_t>((int64_t)c.n_exp * 32, e->n_lanes);
+  LAUNCH(KC_MISC, k_exp_pack_signal, grid_for(pw, VB, 148 * 8), VB, c);
+  LAUNCH(KC_MISC, k_p2p_wait_import, 1, 1024, c, (const uint8_t*)e->p2p_recv, sb);
+  if (c.n_imp > 0)
     LAUNCH(KC_MISC, k_imp_copy, grid_for((int64_t)c.n_imp * 32, VB, 1 << 20), VB, c, (const uint8_t*)e->p2p_recv, sb);
-  }
 }
 
 // phase 0 = whole step; 1 = through k_update; 2 = the rest (split mode).
@@ -407,8 +403,8 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   }
   LAUNCH(KC_REGROUP, k_regroup, RG_BLOCKS, 32 * PD_WARPS, c, 0);
   if (fork_rare) cudaStreamWaitEvent(e->cur, e->ev_join3, 0);
-  if (c.sharded) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
-  if (c.sharded && e->p2p_ready) issue_exchange(e, L);
+  if (c.sharded && !e->p2p_ready) LAUNCH(KC_MISC, k_count_own, grid_for(NL, VB, 148 * 8), VB, c);
+  if (c.sharded && e->p2p_ready) issue_exchange(e, L);  // (counts the own vehicles too)
 }
 
 // Accumulates the current snapshot's road aggregate if the next step has not
@@ -1251,7 +1247,7 @@ int tsb_shard_import(tsb_engine* e, const void* recv, const int64_t* bytes) {
   return TSB_OK;
 }
 
-// ---- device-driven exchange over peer memory (kernels.cu k_exp_pack_p2p)
+// ---- device-driven exchange over peer memory (kernels.cu k_exp_pack_signal)
 
 int tsb_shard_p2p_alloc(tsb_engine* e, void** recv, void** flags, int64_t* slot_bytes) {
   if (!e || !e->c.sharded) return fail(TSB_EINVAL, "not a sharded engine");

@@ -3073,22 +3073,93 @@ __global__ void k_exp_pack(Ctx c, uint8_t* send) {
   }
 }
 
-// Device-driven exchange over peer memory (NVLink P2P / CUDA IPC): the pack
-// writes each peer's message straight into that peer's receive slot for this
-// rank and step parity -- the same layout as k_exp_pack's -- then
-// k_p2p_signal publishes the step epoch in the peer's flag for this rank and
-// k_p2p_wait waits for every peer's flag before the import reads the local
-// slots.  Two slot sets by step parity: a rank writes parity t+1 only after
-// its own import of step t saw every peer's step-t flag, which each peer
-// raised after importing step t-1 from that slot set.
-__global__ void k_exp_pack_p2p(Ctx c) {
+// ---- the device-driven exchange in four kernels (issue_exchange)
+//
+// k_exp_prep: export counts and their exclusive scan in one block (the
+// entries are the boundary lanes: a few thousand).  k_exp_pack_signal: the
+// own-vehicle count, the pack into the peers' slots, and -- by the last block
+// to finish, after every block fenced its remote writes -- the release of the
+// peers' arrival flags.  k_p2p_wait_import: the wait for every peer's flag,
+// then the import counts and their scan in one block.  k_imp_copy.
+
+// Block-wide: cnt[i] = count(i), pos[i] = exclusive prefix, pos[n] = total
+// (each thread a contiguous chunk, one block scan of the chunk sums).
+template <class F>
+__device__ void block_count_scan(int32_t n, F count, int32_t* cnt, int32_t* pos) {
+  __shared__ int32_t s_w[32];
+  __shared__ int32_t s_total;
+  const int T = blockDim.x;
+  const int32_t chunk = (n + T - 1) / T;
+  const int32_t a = min(n, (int32_t)threadIdx.x * chunk), b = min(n, a + chunk);
+  int32_t sum = 0;
+  for (int32_t i = a; i < b; i++) {
+    const int32_t v = count(i);
+    cnt[i] = v;
+    sum += v;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < (T >> 5) ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < (T >> 5)) s_w[lane] = w;
+    if (lane == 31) s_total = w;
+  }
+  __syncthreads();
+  int32_t run = (warp ? s_w[warp - 1] : 0) + x - sum;
+  for (int32_t i = a; i < b; i++) {
+    pos[i] = run;
+    run += cnt[i];
+  }
+  if (threadIdx.x == 0) pos[n] = s_total;
+}
+
+__global__ void __launch_bounds__(1024) k_exp_prep(Ctx c) {
   PDL_WAIT();
-  const unsigned long long epoch = c.dyn->xchg_epoch;
-  const VRec* A = c.lay[c.dyn->cur];
+  if (threadIdx.x == 0) c.dyn->xchg_epoch += 1;  // this exchange's epoch (device-side: graph-capturable)
   const int2* S = c.rng[c.dyn->cur];
+  block_count_scan(
+      c.n_exp,
+      [&](int32_t e) {
+        const int2 sg = seg(c, S, c.exp_lane[e]);
+        return c.exp_kind[e] ? 0 : sg.y - sg.x;  // a max-pressure entry carries no records
+      },
+      c.exp_cnt, c.exp_pos);
+}
+
+__global__ void k_exp_pack_signal(Ctx c) {
+  PDL_WAIT();
+  Dyn* dy = c.dyn;
+  const int2* S = c.rng[dy->cur];
+  // own vehicles in the snapshot (vehicle_updates counts them next step)
+  {
+    int32_t mine = 0;
+    for (int32_t L = gtid(); L < c.n_lanes; L += gstride())
+      if (c.zone[L] & ZF_OWN) {
+        const int2 sg = seg(c, S, L);
+        mine += sg.y - sg.x;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&dy->n_own, mine);
+  }
+  // the pack, straight into the peers' receive slots
+  const unsigned long long epoch = dy->xchg_epoch;
+  const VRec* A = c.lay[dy->cur];
   const int lid = threadIdx.x & 31;
   const int64_t slot = (int64_t)((epoch & 1) * c.nranks + c.rank) * c.p2p_slot;
-  if (gtid() == 0) c.dyn->xchg_bytes += (unsigned long long)exp_base(c, c.nranks);  // every peer's message
+  if (gtid() == 0) dy->xchg_bytes += (unsigned long long)exp_base(c, c.nranks);
   for (int32_t e = gtid() >> 5; e < c.n_exp; e += gstride() >> 5) {
     const int q = c.exp_peer[e];
     const int64_t e0 = c.peer_first_exp[q];
@@ -3100,42 +3171,32 @@ __global__ void k_exp_pack_p2p(Ctx c) {
     const int32_t at = seg(c, S, L).x;
     for (int32_t k = lid; k < n; k += 32) dst[k] = A[at + k];
   }
-}
-
-__global__ void k_p2p_signal(Ctx c) {
-  PDL_WAIT();
-  const unsigned long long epoch = c.dyn->xchg_epoch;
-  __threadfence_system();  // the pack's remote writes before the flags
-  const int q = threadIdx.x;
-  if (q < c.nranks && q != c.rank) {
-    unsigned long long* f = c.p2p_peer_flag[q] + (epoch & 1) * c.nranks + c.rank;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
-  }
-}
-
-__global__ void k_p2p_wait(Ctx c) {
-  PDL_WAIT();
-  const unsigned long long epoch = c.dyn->xchg_epoch;
-  const int q = threadIdx.x;
-  if (q < c.nranks && q != c.rank) {
-    const unsigned long long* f = c.p2p_flag + (epoch & 1) * c.nranks + q;
-    unsigned long long v, t_start, t_now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-      if (v >= epoch) break;
-      __nanosleep(256);
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-      if (t_now - t_start > c.p2p_timeout_ns) {  // a peer stopped stepping: fail loudly, do not hang
-        atomicOr(&c.dyn->overflow, 128);
-        break;
-      }
+  // the last block releases the peers' flags once every block's remote
+  // writes are visible system-wide (each writer fenced before arriving)
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0)
+    s_last = (atomicAdd(&dy->xchg_packed, 1ULL) % (unsigned long long)gridDim.x) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence_system();
+    const int q = threadIdx.x;
+    if (q < c.nranks && q != c.rank) {
+      unsigned long long* f = c.p2p_peer_flag[q] + (epoch & 1) * c.nranks + c.rank;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
     }
   }
-  __syncthreads();
-  __threadfence_system();
 }
 
+// Device-driven exchange over peer memory (NVLink P2P / CUDA IPC): the pack
+// writes each peer's message straight into that peer's receive slot for this
+// rank and step parity -- the same layout as k_exp_pack's -- then the step
+// epoch is released in the peer's flag for this rank and every peer's flag is
+// awaited before the import reads the local slots (k_exp_pack_signal,
+// k_p2p_wait_import below).  Two slot sets by step parity: a rank writes parity t+1 only after
+// its own import of step t saw every peer's step-t flag, which each peer
+// raised after importing step t-1 from that slot set.
 // Receive side: counts from the headers (src_base[q] = byte offset of
 // source q's message in the receive buffer).
 struct SrcBase {
@@ -3160,6 +3221,44 @@ __global__ void k_imp_count(Ctx c, const uint8_t* recv, SrcBase sb) {
       c.imp_cnt[e] = h;
     }
   }
+}
+
+// Wait for every peer's arrival flag, then the import counts
+// from the headers and their scan, in one block (k_imp_count + scan).
+__global__ void __launch_bounds__(1024) k_p2p_wait_import(Ctx c, const uint8_t* recv, SrcBase sb) {
+  PDL_WAIT();
+  const unsigned long long epoch = c.dyn->xchg_epoch;
+  const int q = threadIdx.x;
+  if (q < c.nranks && q != c.rank) {
+    const unsigned long long* f = c.p2p_flag + (epoch & 1) * c.nranks + q;
+    unsigned long long v, t_start, t_now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+      if (t_now - t_start > c.p2p_timeout_ns) {  // a peer stopped stepping: fail loudly, do not hang
+        atomicOr(&c.dyn->overflow, 128);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+  block_count_scan(
+      c.n_imp,
+      [&](int32_t e) {
+        const int qq = c.imp_peer[e];
+        const int32_t h = ((const int32_t*)(recv + src_base(c, sb, qq)))[e - c.peer_first_imp[qq]];
+        if (c.imp_kind[e]) {  // the owner's post-sweep count of a max-pressure lane
+          c.lane_counts[c.imp_lane[e]] = h;
+          return 0;
+        }
+        return h;
+      },
+      c.imp_cnt, c.imp_pos);
+  if (threadIdx.x == 0 && c.n_imp == 0) c.dyn->n_g = 0;
 }
 
 // Warp per import entry: ghost range of the lane, records appended after the
