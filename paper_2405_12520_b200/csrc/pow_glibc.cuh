@@ -30,6 +30,10 @@
 // zero included), finite y.  Anything else returns NaN (never reached: the
 // model's bases are a speed ratio and a gap ratio).
 #pragma once
+// the overflow / underflow results below are intended (glibc builds them the same way)
+#ifdef __CUDACC__
+#pragma nv_diag_suppress 222
+#endif
 #include <cstdint>
 #include <cstring>
 
