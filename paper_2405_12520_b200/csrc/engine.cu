@@ -709,21 +709,7 @@ static int capture_steps(tsb_engine* e, int copies, cudaGraph_t* graph, cudaGrap
 // The step graph (one step) and the batch graph (STEPS_PER_BATCH steps: the
 // launch gap between graph replays, ~10 us, is paid once per batch).
 static constexpr int STEPS_PER_BATCH = 4;
-// Kernels without (much) shared memory get the whole unified L1/shared
-// array as L1 (UPD_L1_CARVEOUT: the carve-out preference, percent shared).
-#ifndef UPD_L1_CARVEOUT
-#define UPD_L1_CARVEOUT -1
-#endif
-static void set_carveouts() {
-  if (UPD_L1_CARVEOUT < 0) return;
-  cudaFuncSetAttribute(k_update<false>, cudaFuncAttributePreferredSharedMemoryCarveout, UPD_L1_CARVEOUT);
-  cudaFuncSetAttribute(k_update<true>, cudaFuncAttributePreferredSharedMemoryCarveout, UPD_L1_CARVEOUT);
-  cudaFuncSetAttribute(k_place, cudaFuncAttributePreferredSharedMemoryCarveout, UPD_L1_CARVEOUT);
-  cudaGetLastError();
-}
-
 static int build_graph(tsb_engine* e) {
-  set_carveouts();
   int n1 = 0, n4 = 0;
   RC(capture_steps(e, 1, &e->graph, &e->gexec, &n1));
   RC(capture_steps(e, STEPS_PER_BATCH, &e->graph4, &e->gexec4, &n4));
