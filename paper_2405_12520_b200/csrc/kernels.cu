@@ -2163,18 +2163,28 @@ __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
     printf("RF step %lld ev %d/%d E %d qn %d edges %d lanes_touched %d reverts %lld bfs %llu replay %llu wait+publish %llu ns\n",
            (long long)dy->step_no, ev, ne, E, qn, nedge, R.nt, (long long)R.reverts, t1 - t0, t2 - t1, t3 - t2);
 #endif
+  // publish the bookkeeping with the whole warp: the touched lanes' dirty
+  // marks and the moved list in parallel (lane 0's serial atomics were a
+  // chain of dependent round trips)
+  const int32_t nt = __shfl_sync(0xffffffffu, R.nt, 0);
+  const int32_t nmv = __shfl_sync(0xffffffffu, R.nmoved, 0);
+  if (staged) {
+    for (int32_t k = lid; k < nt; k += 32) mark_dirty(c, R.touched[k]);  // no global flags to clear
+  } else if (lid == 0) {
+    replay_finish(c, R);
+  }
+  int32_t base = 0;
   if (lid == 0) {
-    if (staged) {
-      for (int32_t k = 0; k < R.nt; k++) mark_dirty(c, R.touched[k]);  // no global flags to clear
-    } else {
-      replay_finish(c, R);
-    }
     if (c.sharded && R.zf == 3) dy->overflow |= 16;
-    const int32_t base = atomicAdd(&dy->n_moved, R.nmoved);
-    for (int32_t k = 0; k < R.nmoved; k++) c.rs_moved[base + k] = R.moved[k];
+    base = atomicAdd(&dy->n_moved, R.nmoved);
     atomicAdd((unsigned long long*)&dy->reverts_last, (unsigned long long)R.reverts);
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int32_t k = lid; k < nmv; k += 32) c.rs_moved[base + k] = R.moved[k];
+  __threadfence();  // every lane's writes before the warp's arrival below
+  __syncwarp();
+  if (lid == 0) {
     // the last replay to finish sees the final dirty / moved counts
-    __threadfence();
     if (atomicAdd(&dy->rf_fin, 1) == ne - 1) {
       __threadfence();
       rare_if_unpatchable(c);
