@@ -288,6 +288,9 @@ __device__ __forceinline__ void count_bucket(const Ctx& c, int32_t lane, int32_t
 #ifndef UPD_GRID_CAP
 #define UPD_GRID_CAP (1 << 30)
 #endif
+#ifndef PLACE_A0
+#define PLACE_A0 1  // 1: B.src carries the snapshot lane's range start from k_update to k_place
+#endif
 #ifndef MOBIL_UNROLL
 #define MOBIL_UNROLL 2
 #endif
@@ -618,7 +621,14 @@ __global__ void __launch_bounds__(UPD_BT, UPD_MINB) k_update(Ctx c) {
         LT = c.lanes[nl];
       }
     }
+#if PLACE_A0
+    // B's src field is the record's own index (implied by its position): it
+    // carries the snapshot lane's range start instead, which k_place needs
+    // for a stayer's rank (one dependent load less there); k_place restores src
+    VRec out{ns, nv, me.vix, nptr, nl, sg0.x};
+#else
     VRec out{ns, nv, me.vix, nptr, nl, i};
+#endif
     nrc_cur[i] = make_int2(nptr, nxt_rd);
     if (arrived && ghost) {  // the owner records it
       out.lane = -1;
@@ -988,7 +998,7 @@ __global__ void k_place(Ctx c) {
     const int32_t base = bbase + (threadIdx.x & ~31);
     const int32_t j = base + lid;
     const bool valid = j < n;
-    const VRec r = valid ? load_b(&c.B[j]) : VRec{0.0, 0.0, 0, 0, -1, 0};
+    VRec r = valid ? load_b(&c.B[j]) : VRec{0.0, 0.0, 0, 0, -1, 0};
     const bool st = valid && c.stay[j];
     const unsigned stay_bits = __ballot_sync(0xffffffffu, st);
     const int32_t L = r.lane;
@@ -996,7 +1006,12 @@ __global__ void k_place(Ctx c) {
     // [a0, j): inside the warp from the ballot; before the warp only for the
     // lane whose range covers `base` -- the first stayer's lane, if its range
     // starts before the warp -- counted by the whole warp, 32 at a time
+#if PLACE_A0
+    const int32_t a0 = st ? r.src : 0;  // the snapshot lane's range start (k_update)
+    r.src = j;                          // C records point at their snapshot record
+#else
     const int32_t a0 = st ? seg(c, SA, L).x : 0;
+#endif
     const int first_st = stay_bits ? __ffs(stay_bits) - 1 : 0;
     const int32_t Ls = __shfl_sync(0xffffffffu, L, first_st);
     const int32_t a0s = __shfl_sync(0xffffffffu, a0, first_st);
