@@ -47,6 +47,12 @@ static int fail(int code, const char* fmt, ...) {
 #define SCAN_IPT_CFG 8
 #endif
 static const int SCAN_BT = 256, SCAN_IPT = SCAN_IPT_CFG, SCAN_TILE = SCAN_BT * SCAN_IPT;
+#ifndef SPEEDS_AT
+#define SPEEDS_AT 0
+#endif
+#ifndef SPEEDS_BLOCKS
+#define SPEEDS_BLOCKS (1 << 30)  // k_speeds grid cap (blocks of 8 warps)
+#endif
 static_assert(SCAN_TILE == LANE_TILE, "k_update sums lane-scan tiles of SCAN_TILE lanes");
 
 enum KernelClass {
@@ -291,18 +297,24 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
   const int jgrid = grid_for(std::max(e->n_junc, 1), VB, 148 * 4);
   const int cgrid = grid_for(std::max(c.n_conn, 1), VB, 148 * 8);
   const int32_t NL = e->n_lanes;
-  if (phase != 2) {
-    LAUNCH(KC_MISC, k_begin_step, grid_for(NL, VB, 148 * 4), VB, c);  // + zeroes the lane counts
-    // previous step's road aggregate on a parallel branch (joined before the regroup)
+  // the snapshot's road aggregate (the previous step's _accumulate_speeds) on a
+  // parallel branch, joined before the regroup; it reads only the snapshot A,
+  // which nothing writes before the regroup.  SPEEDS_AT picks the fork point:
+  // 0 the step's start, 1 after k_lanefix (beside the latency-bound revert
+  // resolution, where SMs are idle), 2 after k_place
+  const int speeds_at = phase == 0 ? SPEEDS_AT : 0;
+  auto fork_speeds = [&]() {
     cudaEventRecord(e->ev_fork, e->cur);
     cudaStreamWaitEvent(e->side, e->ev_fork, 0);
-    {
-      cudaStream_t main_s = e->cur;
-      e->cur = e->side;
-      LAUNCH(KC_SPEEDS, k_speeds, grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, 1 << 30), 256, c, 0);
-      e->cur = main_s;
-    }
+    cudaStream_t main_s = e->cur;
+    e->cur = e->side;
+    LAUNCH(KC_SPEEDS, k_speeds, grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, SPEEDS_BLOCKS), 256, c, 0);
+    e->cur = main_s;
     cudaEventRecord(e->ev_join, e->side);
+  };
+  if (phase != 2) {
+    LAUNCH(KC_MISC, k_begin_step, grid_for(NL, VB, 148 * 4), VB, c);  // + zeroes the lane counts
+    if (speeds_at == 0) fork_speeds();
     if (c.sharded && c.p.controller == 1) {
       // max-pressure decisions of the previous step, from the exchanged counts
       LAUNCH(KC_SIGNALS, k_signals, jgrid, VB, c, (int)SIG_DEFERRED);
@@ -326,7 +338,9 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
            (const int32_t*)c.scan_tile_sums);
   }
   LAUNCH(KC_PLACE, k_place, vgrid, VB, c);
+  if (speeds_at == 2) fork_speeds();
   LAUNCH(KC_LANEFIX, k_lanefix, 148 * LX_BLOCKS_PER_SM, 32 * LX_WARPS, c);
+  if (speeds_at == 1) fork_speeds();
   // Fixed-time signals, the clock and the due list do not depend on vehicle
   // positions: with a fixed-time controller they run on a parallel branch
   // beside the revert resolution (joined before the injection section).

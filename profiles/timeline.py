@@ -19,7 +19,7 @@ from paper_2405_12520_b200 import EngineConfig, World, _native  # noqa: E402
 PH = ["begin", "update", "scan", "place", "lanefix", "resolve_fast", "regroup", "end", "speeds", "signals",
       "inject_due"]
 n = int(os.environ.get("TSB_VEHICLES", "1000000"))
-net, flat, trips, ft = bench.build_workload(n, 29.0)
+net, flat, trips, ft, _ = bench.build_workload(n, 29.0)
 w = World.from_flat(flat, ft, EngineConfig(), seed=42, pow_mode=int(os.environ.get("TSB_POW", "0")))
 L = _native.lib()
 if os.environ.get("TSB_DEBUG"):
@@ -35,7 +35,9 @@ for k, name in enumerate(PH):
     if vals:
         off[name] = round(float(np.median(vals)), 2)
 dur, period = bench.phase_durations(rows)
-out = {"phase_start_us_median": off,
+pct = {k: [round(float(np.percentile(v, q)), 1) for q in (10, 50, 90)] for k, v in dur.items()}
+starts = {name: [round((r[k] - r[0]) / 1000.0, 1) if r[k] > 0 else None for r in rows[:8]] for k, name in enumerate(PH)}
+out = {"phase_start_us_median": off, "phase_us_p10_p50_p90": pct, "first_8_steps_phase_starts_us": starts,
        "phase_us_median": {k: round(float(np.median(v)), 2) for k, v in dur.items()},
        "step_period_us_median": round(float(np.median(period)), 2), "steps": len(rows)}
 print(json.dumps(out))
