@@ -12,8 +12,10 @@ Arms:
   default           the B200 engine (one CUDA graph per step).  Under torchrun
                     with N > 1 ranks: the sharded engine (sharded.py) -- the
                     same 1M-vehicle network split into N spatial lane bands,
-                    one GPU each, ghost lanes exchanged every step with an
-                    NCCL all-to-all (strong scaling: total work fixed)
+                    one GPU each, ghost lanes exchanged every step over
+                    IPC-mapped peer memory (--exchange p2p, default) or an
+                    NCCL all-to-all (strong scaling: total work fixed;
+                    --weak: 1M vehicles per GPU on a (100 N) x 100 grid)
   --impl reference  the reference algorithm on the host CPU: the C port in
                     oracle/ (the reference itself is pure Python and cannot
                     travel to the GPU box), rank 0 only.
