@@ -141,15 +141,16 @@ def test_m1_bench_workload_first_steps():
 
 
 def test_m1_into_the_revert_regime():
-    """The bench workload at full size (1M vehicles) through step 20, where
-    revert chains have started (~20 per step): every StepReport counter each
-    step and the whole lane-sorted state at the end, bit for bit against the
-    CPU oracle in the reference's arithmetic (glibc pow)."""
+    """The bench workload at full size (1M vehicles) through step 100, deep in
+    the revert regime (~25 reverts per step): every StepReport counter each
+    step and the whole lane-sorted state every 25 steps, bit for bit against
+    the CPU oracle in the reference's arithmetic (glibc pow).  (A one-off
+    200-step run plus 3 steps at C5 scale: profiles/round2/long_parity_*.log.)"""
     net = generate_grid(100, 100, block_length=400.0, lanes_per_direction=3)
     router = Router(net)
     trips = preplaced_trips(net, router, 1_000_000, 29.0)
     router.close()
-    g, r, reverts = run_pair(net, trips, EngineConfig(), 42, 20, every=10)
-    assert reverts > 50
-    print("reverts in 20 steps:", reverts)
+    g, r, reverts = run_pair(net, trips, EngineConfig(), 42, 100, every=25)
+    assert reverts > 1000
+    print("reverts in 100 steps:", reverts)
     _close(g, r)
