@@ -97,3 +97,44 @@ def test_m1_queries_at_bench_size():
         print(f"M1 records_arrays ({len(r['vix'])} records): {1e3 * (time.perf_counter() - t0):.1f} ms")
     finally:
         g.close()
+
+
+def test_query_edge_cases():
+    """No trips at all; an unknown id (InputError, world.py:706-709); waiting
+    and dropped vehicles report their origin (world.py:196-198)."""
+    from paper_2405_12520_b200 import InputError, Trip
+
+    net = generate_grid(3, 3)
+    w = World(net, [], EngineConfig(), seed=1)
+    try:
+        w.run(3)
+        assert w.records_arrays()["vix"].size == 0 and w.driving_count() == 0
+        with pytest.raises(InputError):
+            w.get_vehicle(0)
+    finally:
+        w.close()
+    lanes = sorted(net.road_lane_ids())
+    # trip 1 departs later (waiting), trip 2 drives, trip 3's destination lane
+    # is closed before it departs (unroutable: dropped)
+    trips = [Trip(1, lanes[0], 0.0, lanes[-1], 500.0), Trip(2, lanes[1], 3.0, lanes[-2], 0.0),
+             Trip(3, lanes[2], 7.0, lanes[-3], 2.0)]
+    w = World(net, trips, EngineConfig(), seed=1)
+    r = OracleWorld(net, trips, EngineConfig(), seed=1, pow_mode=1)
+    try:
+        w.set_lane_restriction(lanes[-3], "closed")
+        r.set_lane(lanes[-3], float(net.lanes[lanes[-3]].max_speed), False)
+        for _ in range(5):
+            w.step()
+            r.step(1)
+        sv = w.get_vehicle(1)
+        assert sv.status == "waiting" and sv.lane_id == lanes[0] and sv.s == 0.0 and sv.v == 0.0
+        assert sv.route_index == 0 and sv.finish_time is None
+        d = w.get_vehicle(3)
+        assert d.status == "dropped" and d.lane_id == lanes[2] and d.s == 7.0 and d.finish_time is None
+        assert w.get_vehicle(2).status == "driving" and w.dropped == 1
+        rec = CollectingRecorder()
+        w.record_step(rec)
+        assert rec.records == r.records()
+    finally:
+        w.close()
+        r.close()
