@@ -48,7 +48,7 @@ static constexpr double EPS_GAP = 1e-6;  // world.py:43
 static constexpr int TL_SLOTS = 16;
 static constexpr int TL_ROWS = 1024;
 enum { TL_BEGIN, TL_UPDATE, TL_SCAN, TL_PLACE, TL_LANEFIX, TL_RESOLVE, TL_REGROUP, TL_END, TL_SPEEDS, TL_SIGNALS,
-       TL_INJECT_DUE, TL_SPEEDS_END };
+       TL_INJECT_DUE, TL_SPEEDS_END, TL_RESOLVE_END, TL_INJECT_DUE_END };
 #define TL_MARK(k)                                                                        \
   do {                                                                                    \
     if (c.tl_on && blockIdx.x == 0 && threadIdx.x == 0) {                                 \
@@ -57,6 +57,20 @@ enum { TL_BEGIN, TL_UPDATE, TL_SCAN, TL_PLACE, TL_LANEFIX, TL_RESOLVE, TL_REGROU
       c.tl[(size_t)(c.dyn->tl_row & (TL_ROWS - 1)) * TL_SLOTS + (k)] = t_;                \
     }                                                                                     \
   } while (0)
+
+// Stamps slot k when the kernel's block 0 thread 0 leaves the scope (every
+// return path): the approximate end of a kernel whose block 0 finishes last.
+struct TlEnd {
+  const Ctx& c;
+  int k;
+  __device__ ~TlEnd() {
+    if (c.tl_on && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t_;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+      c.tl[(size_t)(c.dyn->tl_row & (TL_ROWS - 1)) * TL_SLOTS + k] = t_;
+    }
+  }
+};
 
 __device__ __forceinline__ int gtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * blockDim.x; }
@@ -2000,6 +2014,7 @@ static constexpr unsigned long long RF_WAIT_NS = 2000000ULL;  // 2 ms (the wait 
 __global__ void __launch_bounds__(32 * RC_WARPS) k_resolve_fast(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_RESOLVE);
+  TlEnd tl_end{c, TL_RESOLVE_END};
   Dyn* dy = c.dyn;
   const int32_t ne = dy->n_events;
   if (ne == 0) {
@@ -2372,6 +2387,7 @@ __global__ void k_conn_flags(Ctx c) {
 __global__ void k_inject_due(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_INJECT_DUE);
+  TlEnd tl_end{c, TL_INJECT_DUE_END};
   Dyn* dy = c.dyn;
   __shared__ int32_t s_new;
   const int32_t nr = dy->n_retry;

@@ -17,7 +17,7 @@ import bench  # noqa: E402
 from paper_2405_12520_b200 import EngineConfig, World, _native  # noqa: E402
 
 PH = ["begin", "update", "scan", "place", "lanefix", "resolve_fast", "regroup", "end", "speeds", "signals",
-      "inject_due"]
+      "inject_due", "speeds_end", "resolve_fast_end", "inject_due_end"]
 n = int(os.environ.get("TSB_VEHICLES", "1000000"))
 net, flat, trips, ft, _ = bench.build_workload(n, 29.0)
 w = World.from_flat(flat, ft, EngineConfig(), seed=42, pow_mode=int(os.environ.get("TSB_POW", "0")))
