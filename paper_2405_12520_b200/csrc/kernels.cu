@@ -1107,8 +1107,19 @@ __global__ void k_place(Ctx c) {
 #ifndef LX_CAP_CFG
 #define LX_CAP_CFG 64
 #endif
-static constexpr int LX_CAP = LX_CAP_CFG;  // lane members staged in shared memory
+// LX_G threads per flagged lane: 16 = two lanes in flight per warp, each
+// group with half the warp's shared-memory staging (32 members on chip; M1's
+// flagged lanes hold <= 32, larger ones stage in global memory).  A/B at M1
+// (r2): 32 -> 16 takes k_lanefix 17.7 -> 16.0 us; 8 threads: 19.9 us.
+#ifndef LX_G
+#define LX_G 16
+#endif
+static constexpr int LX_GPW = 32 / LX_G;               // lanes in flight per warp
+static constexpr int LX_CAP = LX_CAP_CFG / LX_GPW;     // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
+#if !PLACE_LIST && LX_G != 32
+#error "LX_G < 32 needs PLACE_LIST"
+#endif
 // k_lanefix grid: blocks per SM (grid-stride over the flagged lanes); 5 is
 // what fits at once (shared memory), so the launch is one full wave
 #ifndef LX_BLOCKS_PER_SM
@@ -1117,25 +1128,28 @@ static constexpr int LX_WARPS = 8;
 __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_LANEFIX);
-  __shared__ VRec s_in[LX_WARPS][LX_CAP];
-  __shared__ VRec s_out[LX_WARPS][LX_CAP];
-  __shared__ double s_snap_s[LX_WARPS][LX_CAP];
-  __shared__ int32_t s_snap_l[LX_WARPS][LX_CAP];
+  __shared__ VRec s_in[LX_WARPS * LX_GPW][LX_CAP];
+  __shared__ VRec s_out[LX_WARPS * LX_GPW][LX_CAP];
+  __shared__ double s_snap_s[LX_WARPS * LX_GPW][LX_CAP];
+  __shared__ int32_t s_snap_l[LX_WARPS * LX_GPW][LX_CAP];
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
   const VRec* A = c.lay[dy->cur];
-  const int w = threadIdx.x >> 5, lid = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lid = threadIdx.x & 31;
+  const int gi = lid / LX_G, gl = lid % LX_G;  // group in the warp, thread in the group
+  const int w = (threadIdx.x >> 5) * LX_GPW + gi;  // this group's staging slot
+  const unsigned gmask = LX_G == 32 ? 0xffffffffu : (((1u << LX_G) - 1u) << (gi * LX_G));
+  const int groups = ((gridDim.x * blockDim.x) >> 5) * LX_GPW;
   const Params& p = c.p;
 #if PLACE_LIST
   const int32_t nfix = dy->n_fix;
-  for (int32_t f = gtid() >> 5; f < nfix; f += warps) {
+  for (int32_t f = (gtid() >> 5) * LX_GPW + gi; f < nfix; f += groups) {
     const int32_t L = c.fix_list[f];
 #else
   // the flagged lanes: each warp takes 32 lanes' flag words at a time
   const int32_t ngrp = (c.n_lanes + 31) >> 5;
-  for (int32_t g = gtid() >> 5; g < ngrp; g += warps) {
+  for (int32_t g = gtid() >> 5; g < ngrp; g += groups) {
    const int32_t Lg = (g << 5) + lid;
    unsigned todo = __ballot_sync(0xffffffffu, Lg < c.n_lanes && c.fix_flag[Lg]);
    while (todo) {
@@ -1143,46 +1157,46 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
     todo &= todo - 1;
 #endif
     const int32_t lo = CS[L], n = CS[L + 1] - lo;
-    if (lid == 0) {
+    if (gl == 0) {
       c.fix_flag[L] = 0;
       c.ent[L] = 0;  // consumed: zero for the next step (no memsets)
     }
     const bool on_chip = n <= LX_CAP;
     VRec* in = on_chip ? s_in[w] : c.D + lo;  // oversized lanes stage in D
     VRec* out = on_chip ? s_out[w] : C + lo;
-    for (int32_t q = lid; q < n; q += 32) in[q] = C[lo + q];
-    __syncwarp();
+    for (int32_t q = gl; q < n; q += LX_G) in[q] = C[lo + q];
+    __syncwarp(gmask);
     // rank sort (keys unique: vix distinct)
-    for (int a = lid; a < n; a += 32) {
+    for (int a = gl; a < n; a += LX_G) {
       const double sa = in[a].s;
       const int32_t va = in[a].vix;
       int rank = 0;
       for (int b2 = 0; b2 < n; b2++) rank += ahead_of(in[b2].s, in[b2].vix, sa, va) ? 1 : 0;
       out[rank] = in[a];
     }
-    __syncwarp();
-    // tentative sweep: parallel trigger test, then lane 0 from the first trigger
+    __syncwarp(gmask);
+    // tentative sweep: parallel trigger test, then thread 0 from the first trigger
     int32_t first = n;
-    for (int32_t j = lid; j < n; j += 32) {
+    for (int32_t j = gl; j < n; j += LX_G) {
       if (j == 0) continue;
       const double limit = (out[j - 1].s - p.L) - p.s0_floor;
       if (out[j].s > limit + 1e-12) first = min(first, j);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    for (int o = LX_G / 2; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(gmask, first, o, LX_G));
     // the sweep reads each member's snapshot lane / s: gathered in parallel
-    // first (on-chip lanes), not one dependent load per member in lane 0
+    // first (on-chip lanes), not one dependent load per member in thread 0
     const bool pre = on_chip && first < n;
     if (pre) {
-      for (int32_t q = first - 1 + lid; q < n; q += 32) {
+      for (int32_t q = first - 1 + gl; q < n; q += LX_G) {
         const VRec sn = A[out[q].src];
         s_snap_l[w][q] = sn.lane;
         s_snap_s[w][q] = sn.s;
       }
-      __syncwarp();
+      __syncwarp(gmask);
     }
     int32_t q_ev = -1;  // event: members [first, q_ev) were clamped and are restored
-    if (first < n && lid == 0) {
+    if (first < n && gl == 0) {
       VRec prev = out[first - 1];
       bool prev_entered = prev.lane != (pre ? s_snap_l[w][first - 1] : A[prev.src].lane);
       double prev_rear = prev.s - p.L;
@@ -1232,20 +1246,20 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
           }
       }
     }
-    q_ev = __shfl_sync(0xffffffffu, q_ev, 0);
-    __syncwarp();
+    q_ev = __shfl_sync(gmask, q_ev, 0, LX_G);
+    __syncwarp(gmask);
     if (q_ev >= 0) {
       // leave the lane unswept (post-delta values) for the replay
-      for (int32_t u = first + lid; u < q_ev; u += 32) {
+      for (int32_t u = first + gl; u < q_ev; u += LX_G) {
         const VRec o = c.B[out[u].src];
         out[u].s = o.s;
         out[u].v = o.v;
       }
     }
-    __syncwarp();
+    __syncwarp(gmask);
     if (on_chip)
-      for (int a = lid; a < n; a += 32) C[lo + a] = out[a];
-    __syncwarp();
+      for (int a = gl; a < n; a += LX_G) C[lo + a] = out[a];
+    __syncwarp(gmask);
 #if !PLACE_LIST
    }
 #endif
