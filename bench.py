@@ -461,8 +461,11 @@ def main():
         updates = r.vehicle_updates - u0
         barrier(pg)
         # end-to-end through the public API: World.step() per step, each step
-        # reading its StepReport back to the host
-        e2e_steps = max(10, args.steps // 4)
+        # reading its StepReport back to the host (two untimed calls first:
+        # the switch from the batch graph to the one-step graph)
+        world.step()
+        world.step()
+        e2e_steps = max(20, args.steps)
         u1 = world.vehicle_updates
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
@@ -543,7 +546,7 @@ def main():
                    "paths_per_timed_step": {k: (pc1[i] - pc0[i]) / args.steps for i, k in enumerate(PATHS)},
                    "sequential_resolve_steps": r_end.resolve_sequential, "steps_total": r_end.step_no},
         "e2e": {"value": e2e_rate, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": sync_bytes.value,
+                "d2h_bytes_per_step": sync_bytes.value, "steps": e2e_steps,
                 "how": "World.step() loop (reference API), wall clock; each step waits for and reads the "
                        "step scalars (StepReport counters + error flags), which the step's last block writes "
                        "into mapped host memory (zero-copy D2H); a stateful "

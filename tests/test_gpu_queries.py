@@ -116,7 +116,7 @@ def test_query_edge_cases():
     lanes = sorted(net.road_lane_ids())
     # trip 1 departs later (waiting), trip 2 drives, trip 3's destination lane
     # is closed before it departs (unroutable: dropped)
-    trips = [Trip(1, lanes[0], 0.0, lanes[-1], 500.0), Trip(2, lanes[1], 3.0, lanes[-2], 0.0),
+    trips = [Trip(1, lanes[0], 0.0, lanes[-1], 500.0), Trip(2, lanes[1], 3.0, lanes[-1], 0.0),
              Trip(3, lanes[2], 7.0, lanes[-3], 2.0)]
     w = World(net, trips, EngineConfig(), seed=1)
     r = OracleWorld(net, trips, EngineConfig(), seed=1, pow_mode=1)
@@ -132,6 +132,8 @@ def test_query_edge_cases():
         d = w.get_vehicle(3)
         assert d.status == "dropped" and d.lane_id == lanes[2] and d.s == 7.0 and d.finish_time is None
         assert w.get_vehicle(2).status == "driving" and w.dropped == 1
+        st, _, _ = r.status()
+        assert [w.get_vehicle(t.id).status for t in trips] == [_ST[int(x)] for x in st]
         rec = CollectingRecorder()
         w.record_step(rec)
         assert rec.records == r.records()
