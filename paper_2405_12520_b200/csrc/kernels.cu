@@ -1114,24 +1114,36 @@ __global__ void k_place(Ctx c) {
 #ifndef LX_G
 #define LX_G 16
 #endif
+// LX_REUSE: the snapshot (s, lane) of a swept lane's members go into the
+// unsorted copy's shared memory (dead after the sort): 32 KB per block, so
+// with <= 40 registers (LX_MINB) six blocks fit per SM.  A/B at M1 (r2):
+// k_lanefix 19.2 -> 17.2 us, the step -1.6 us; the reuse alone at 5 blocks: -0.5.
+#ifndef LX_REUSE
+#define LX_REUSE 1
+#endif
 static constexpr int LX_GPW = 32 / LX_G;               // lanes in flight per warp
 static constexpr int LX_CAP = LX_CAP_CFG / LX_GPW;     // lane members staged in shared memory
 static constexpr int LX_WARPS = 8;
 #if !PLACE_LIST && LX_G != 32
 #error "LX_G < 32 needs PLACE_LIST"
 #endif
-// k_lanefix grid: blocks per SM (grid-stride over the flagged lanes); 5 is
-// what fits at once (shared memory), so the launch is one full wave
+// k_lanefix grid: blocks per SM (grid-stride over the flagged lanes); 6 is
+// what fits at once (shared memory, registers), so the launch is one full wave
 #ifndef LX_BLOCKS_PER_SM
-#define LX_BLOCKS_PER_SM 5
+#define LX_BLOCKS_PER_SM 6
 #endif
-__global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
+#ifndef LX_MINB
+#define LX_MINB LX_BLOCKS_PER_SM
+#endif
+__global__ void __launch_bounds__(32 * LX_WARPS, LX_MINB) k_lanefix(Ctx c) {
   PDL_WAIT();
   TL_MARK(TL_LANEFIX);
   __shared__ VRec s_in[LX_WARPS * LX_GPW][LX_CAP];
   __shared__ VRec s_out[LX_WARPS * LX_GPW][LX_CAP];
+#if !LX_REUSE
   __shared__ double s_snap_s[LX_WARPS * LX_GPW][LX_CAP];
   __shared__ int32_t s_snap_l[LX_WARPS * LX_GPW][LX_CAP];
+#endif
   Dyn* dy = c.dyn;
   VRec* C = c.lay[dy->cur ^ 1];
   const int32_t* CS = c.start[dy->cur ^ 1];
@@ -1140,6 +1152,15 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
   const int gi = lid / LX_G, gl = lid % LX_G;  // group in the warp, thread in the group
   const int w = (threadIdx.x >> 5) * LX_GPW + gi;  // this group's staging slot
   const unsigned gmask = LX_G == 32 ? 0xffffffffu : (((1u << LX_G) - 1u) << (gi * LX_G));
+#if LX_REUSE
+  // the members' snapshot (s, lane) in the unsorted copy's storage, dead
+  // after the rank sort (12 of its 32 bytes per member)
+  double* const snap_s = reinterpret_cast<double*>(&s_in[w][0]);
+  int32_t* const snap_l = reinterpret_cast<int32_t*>(snap_s + LX_CAP);
+#else
+  double* const snap_s = s_snap_s[w];
+  int32_t* const snap_l = s_snap_l[w];
+#endif
   const int groups = ((gridDim.x * blockDim.x) >> 5) * LX_GPW;
   const Params& p = c.p;
 #if PLACE_LIST
@@ -1190,15 +1211,15 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
     if (pre) {
       for (int32_t q = first - 1 + gl; q < n; q += LX_G) {
         const VRec sn = A[out[q].src];
-        s_snap_l[w][q] = sn.lane;
-        s_snap_s[w][q] = sn.s;
+        snap_l[q] = sn.lane;
+        snap_s[q] = sn.s;
       }
       __syncwarp(gmask);
     }
     int32_t q_ev = -1;  // event: members [first, q_ev) were clamped and are restored
     if (first < n && gl == 0) {
       VRec prev = out[first - 1];
-      bool prev_entered = prev.lane != (pre ? s_snap_l[w][first - 1] : A[prev.src].lane);
+      bool prev_entered = prev.lane != (pre ? snap_l[first - 1] : A[prev.src].lane);
       double prev_rear = prev.s - p.L;
       bool event = false;
       int32_t q = first;
@@ -1208,8 +1229,8 @@ __global__ void __launch_bounds__(32 * LX_WARPS) k_lanefix(Ctx c) {
         int32_t sn_lane;
         double sn_s;
         if (pre) {
-          sn_lane = s_snap_l[w][q];
-          sn_s = s_snap_s[w][q];
+          sn_lane = snap_l[q];
+          sn_s = snap_s[q];
         } else {
           const VRec sn = A[r.src];
           sn_lane = sn.lane;
