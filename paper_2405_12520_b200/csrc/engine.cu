@@ -308,7 +308,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
     cudaStreamWaitEvent(e->side, e->ev_fork, 0);
     cudaStream_t main_s = e->cur;
     e->cur = e->side;
-    LAUNCH(KC_SPEEDS, k_speeds, grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, SPEEDS_BLOCKS), 256, c, 0);
+    LAUNCH(KC_SPEEDS, k_speeds, grid_for(SP_G * (int64_t)std::max(e->n_roads, 1), 256, SPEEDS_BLOCKS), 256, c, 0);
     e->cur = main_s;
     cudaEventRecord(e->ev_join, e->side);
   };
@@ -424,7 +424,7 @@ static void issue_step(tsb_engine* e, Launcher& L, int phase) {
 // Accumulates the current snapshot's road aggregate if the next step has not
 // done it yet (k_speeds); called before the aggregate is read.
 static int flush_speeds(tsb_engine* e) {
-  k_speeds<<<grid_for(32 * (int64_t)std::max(e->n_roads, 1), 256, 1 << 30), 256, 0, e->stream>>>(e->c, 1);
+  k_speeds<<<grid_for(SP_G * (int64_t)std::max(e->n_roads, 1), 256, 1 << 30), 256, 0, e->stream>>>(e->c, 1);
   k_speeds_done<<<1, 1, 0, e->stream>>>(e->c);
   CK(cudaGetLastError());
   return TSB_OK;

@@ -2789,6 +2789,13 @@ __global__ void k_full_finish(Ctx c) {
 // the NEXT step on a parallel branch (A is only read until that step's
 // regroup, which joins it); mode 1 is the flush a query issues between
 // steps.  Both use the same order.
+// threads per road in k_speeds: 8 (four roads per warp).  The kernel runs on
+// a side branch beside k_update's last wave and the lane scan; a warp per
+// road held 4x the warps for the same ~3 us of work.  A/B at M1 (r2): 32 ->
+// 8 threads: k_update -3 us, the scan phase -2.8 us, the step -7 us; 4: -6 us.
+#ifndef SP_G
+#define SP_G 8
+#endif
 __global__ void k_speeds(Ctx c, int flush) {
   PDL_WAIT();
   if (!flush) TL_MARK(TL_SPEEDS);
@@ -2801,25 +2808,26 @@ __global__ void k_speeds(Ctx c, int flush) {
     if (gtid() == 0) dy->overflow |= 2;
     return;
   }
-  // warp per road: a segmented reduction -- the lanes of the warp stride
-  // over the road's lane ranges (road lanes are consecutive ids, each lane's
-  // records one range), then a butterfly sum across the warp; the order is
-  // fixed, so the aggregate is deterministic run to run
-  const int32_t ln = threadIdx.x & 31;
-  const int32_t nw = gstride() >> 5;
-  for (int32_t r = gtid() >> 5; r < c.n_roads; r += nw) {
+  // SP_G threads per road: a segmented reduction -- the group's threads
+  // stride over the road's lane ranges (road lanes are consecutive ids, each
+  // lane's records one range), then a butterfly sum across the group; the
+  // order is fixed, so the aggregate is deterministic run to run
+  const int32_t ln = threadIdx.x % SP_G;
+  const unsigned gmask = SP_G == 32 ? 0xffffffffu : (((1u << SP_G) - 1u) << ((threadIdx.x & 31) / SP_G * SP_G));
+  const int32_t nw = gstride() / SP_G;
+  for (int32_t r = gtid() / SP_G; r < c.n_roads; r += nw) {
     const int2 span = c.road_span[r];
     if (c.sharded && !(c.zone[span.x] & ZF_OWN)) continue;  // the owner accumulates it
     double sum = 0.0;
     int32_t cnt = 0;
     for (int32_t L = span.x; L <= span.y; L++) {
       const int2 sg = seg(c, S, L);
-      for (int32_t j = sg.x + ln; j < sg.y; j += 32) sum += __ldg(&A[j].v);
+      for (int32_t j = sg.x + ln; j < sg.y; j += SP_G) sum += __ldg(&A[j].v);
       cnt += sg.y - sg.x;
     }
     if (cnt == 0) continue;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o = SP_G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, SP_G);
     if (ln == 0) {
       const size_t cell = (size_t)r * c.n_win + wi;
       c.acc_sum[cell] += sum;
